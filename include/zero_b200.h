@@ -1,0 +1,308 @@
+/*
+ * zero_b200.h -- C ABI of the B200-native ZeRO-DP hot path (arXiv 1910.02054).
+ *
+ * The library implements one partitioned mixed-precision Adam step at ZeRO-DP
+ * stage 0 (replicated DP baseline), 1 (P_os), 2 (P_os+g) or 3 (P_os+g+p):
+ *   zero_reduce_grads  flatten/cast/prescale a gradient bucket and reduce-scatter it
+ *                      so rank r holds only its 1/N_d partition (§5.2)
+ *   zero_step          overflow check + global grad norm, fused partitioned Adam on
+ *                      the owned shard with the 16-bit recast written straight into
+ *                      the all-gather buffer, then the all-gather (§5.1)
+ *   zero_gather_params stage 3: per-layer all-gather with prefetch before each
+ *                      forward/backward use (§5.3 and §7.2.2)
+ * Citations "P:n" are lines of the paper text; "c-k" are the readings
+ * recorded in DESIGN.md §3 where the paper is silent.
+ *
+ * Conventions for every call:
+ *  - Every function returns zero_status; nothing throws across the ABI.
+ *  - Pointers documented as "device" are CUDA device (or UVA-mapped) addresses on
+ *    the context's device; "host" pointers are ordinary CPU memory.
+ *  - A context is used by one host thread.  All calls after zero_bind_buffers are
+ *    asynchronous with respect to the host (stream-ordered on the caller's compute
+ *    stream) unless stated otherwise.
+ *  - ZERO_EINVAL: bad argument; no state was changed.
+ *    ZERO_ESTATE: call-order violation (e.g. zero_step before every bucket of the
+ *    step was reduced); no state was changed.
+ *    ZERO_ECUDA / ZERO_ENCCL: a CUDA or NCCL error; the context is poisoned (sticky)
+ *    and every later call except zero_last_error/zero_destroy returns the same code.
+ *  - Gradient overflow is NOT an error: the step is skipped and reported (c-4).
+ */
+#ifndef ZERO_B200_H
+#define ZERO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZERO_ABI_VERSION 1
+#define ZERO_MAX_RANKS 8      /* one NVL8 box */
+
+typedef enum {
+  ZERO_OK = 0,
+  ZERO_EINVAL = 1,
+  ZERO_ENOMEM = 2,
+  ZERO_ECUDA = 3,
+  ZERO_ENCCL = 4,
+  ZERO_ESTATE = 5,
+  ZERO_EUNSUPPORTED = 6
+} zero_status;
+
+/* 16-bit model dtypes (fp16 params/grads, fp32 optimizer states). */
+typedef enum { ZERO_FP16 = 0, ZERO_BF16 = 1, ZERO_FP32 = 2 } zero_dtype;
+
+/* Reduced-gradient precision (reading c-2): R16 = fp32 sum in ascending rank,
+ * rounded once to 16-bit (2 bytes/elem, the paper's 2Psi/N_d); R32 = the
+ * same fp32 sum kept in fp32 (4 bytes/elem). */
+typedef enum { ZERO_R16 = 0, ZERO_R32 = 1 } zero_reduce_mode;
+
+/* How ranks exchange data.
+ * LOCAL: n_d == 1, no collective ("N=1 degenerates").
+ * NCCL:  one process per GPU; ncclReduceScatter / ncclAllGather / ncclAllReduce on a
+ *        communicator borrowed from torch (ProcessGroupNCCL._comm_ptr()).
+ * PEER:  ranks read/write each other's buffers through a peer-pointer table
+ *        (pull reduce-scatter in fixed rank order; the Adam kernel stores the
+ *        recast parameters into every rank's replica = fused all-gather).  The
+ *        table is installed by zero_sim_group (N contexts on one device, one
+ *        process: BASELINE config 1's "simulated ranks"). */
+typedef enum { ZERO_TRANSPORT_LOCAL = 0, ZERO_TRANSPORT_NCCL = 1, ZERO_TRANSPORT_PEER = 2 } zero_transport;
+
+/* ---------------------------------------------------------------------------
+ * Parameter layout (reading c-7; "N_d equal partitions", P:366 buckets,
+ * P:420-422 constant-size buffer C_B).
+ * Tensors are listed in forward order with non-decreasing layer ids.  Tensor t
+ * is placed in buckets that never span layers; every bucket is padded to a
+ * multiple of N_d * align_elems; rank r owns the r-th 1/N_d slice of every
+ * bucket, so each rank owns exactly psi_padded / N_d elements.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  uint64_t numel;   /* elements of the tensor (0 allowed: the tensor is skipped) */
+  uint32_t layer;   /* layer id, non-decreasing in forward order */
+  uint32_t reserved;
+} zero_tensor;
+
+typedef struct {
+  uint32_t n_tensors;
+  uint32_t align_elems;        /* A: power of two >= 1; 64 = 128 B of 16-bit */
+  const zero_tensor* tensors;  /* host array of n_tensors, copied by the callee */
+  uint64_t bucket_cap_elems;   /* C_B in elements; 0 = one bucket per layer */
+} zero_layout_desc;
+
+typedef struct {
+  uint32_t layer;
+  uint32_t n_pieces;
+  uint32_t first_piece;        /* index into the piece array */
+  uint32_t reserved;
+  uint64_t base;               /* global flat offset of the bucket */
+  uint64_t size;               /* B_k: padded size, multiple of N_d * A */
+  uint64_t shard_off;          /* offset of this bucket's slice in every rank's shard */
+} zero_bucket;
+
+typedef struct {
+  uint32_t tensor;
+  uint32_t bucket;
+  uint64_t tensor_off;         /* first element of the tensor covered */
+  uint64_t bucket_off;         /* position inside the bucket (A-aligned) */
+  uint64_t count;
+} zero_piece;
+
+typedef struct {
+  uint64_t psi;                /* true parameter count */
+  uint64_t psi_padded;         /* Psi' = sum of B_k */
+  uint64_t shard;              /* Psi' / N_d */
+  uint32_t n_buckets;
+  uint32_t n_pieces;
+  uint32_t n_layers;           /* number of distinct layer ids that own buckets */
+  uint32_t max_bucket;         /* max B_k (elements) -- fits in 32 bits only when
+                                  C_B is set; 0xFFFFFFFF means "see buckets" */
+} zero_layout_info;
+
+/* Pure host function (no GPU needed).  Computes the layout of `desc` for `n_d`
+ * ranks.  Fills *info; fills `buckets` / `pieces` (host arrays) when non-NULL
+ * and their capacities (cap_buckets, cap_pieces) are large enough, else returns
+ * ZERO_EINVAL after filling *info (call once with NULL arrays to size them).
+ * Errors: ZERO_EINVAL for n_d < 1 or > ZERO_MAX_RANKS, A not a power of two,
+ * 0 < C_B < N_d*A, decreasing layer ids, or a layout with no elements. */
+zero_status zero_plan_layout(const zero_layout_desc* desc, int n_d, zero_layout_info* info,
+                             zero_bucket* buckets, uint32_t cap_buckets,
+                             zero_piece* pieces, uint32_t cap_pieces);
+
+/* ---------------------------------------------------------------------------
+ * Optimizer configuration (copied at zero_init).  Adam as read in c-3:
+ *   g = G * inv (* clip);  m = b1*m + (1-b1)*g;  v = b2*v + ((1-b2)*g)*g;
+ *   p = p - step * (m / (sqrt(v)*rsb2 + eps)),  step = lr/(1-b1^t), rsb2 = 1/sqrt(1-b2^t)
+ * fp32, each op rounded to nearest, no FMA; inv = 1/(N_d * S * prescale).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  float lr, beta1, beta2, eps;
+  float weight_decay;          /* > 0: decoupled p -= lr*wd*p before the update */
+  float max_grad_norm;         /* > 0: clip by max/(norm + 1e-6) when norm > max */
+  zero_dtype param_dtype;      /* FP16 | BF16 */
+  zero_dtype grad_dtype;       /* FP16 | BF16 (must equal param_dtype) | FP32 */
+  zero_reduce_mode reduce_mode;
+  int32_t dynamic_loss_scale;  /* 1: halve on overflow, double after scale_window good steps */
+  float loss_scale;            /* initial S (power of two) */
+  float min_loss_scale;
+  uint32_t scale_window;
+  float grad_prescale;         /* sigma, power of two applied in the flatten (default 1) */
+  uint32_t prefetch_depth;     /* stage 3: layers gathered ahead of use (default 1) */
+  uint32_t pool_buckets;       /* stages 2/3, N_d > 1: C_B staging slots (default 2) */
+  uint32_t timing;             /* 1: record CUDA events around each phase (ZERO_Q_TIMING) */
+} zero_config;
+
+/* Step record (32 bytes), written asynchronously by zero_step. */
+typedef struct {
+  uint64_t t;                  /* Adam step count after this step (unchanged if skipped) */
+  uint32_t overflow;           /* 1: a non-finite reduced gradient -> step skipped */
+  float loss_scale;            /* S used by this step */
+  float clip;                  /* clip coefficient applied (1 = none) */
+  uint32_t reserved;
+  double grad_norm;            /* sqrt(sum (G*inv)^2) over all Psi' elements */
+} zero_step_info;
+
+/* ---------------------------------------------------------------------------
+ * Context lifecycle
+ * ------------------------------------------------------------------------- */
+struct zero_ctx;
+
+/* Create the context of rank `rank` of `n_d`.
+ *  stage: 0 = replicated DP (all-reduce, every rank updates all Psi'),
+ *         1 = P_os, 2 = P_os+g, 3 = P_os+g+p.
+ *  K: optimizer bytes per parameter; must be 12 ("Mixed-precision Adam has K=12").
+ *  transport: LOCAL requires n_d == 1; NCCL requires nccl_comm (an ncclComm_t of
+ *  size n_d whose rank is `rank`, borrowed, never destroyed); PEER requires a later
+ *  zero_sim_group.  compute_stream: cudaStream_t (borrowed; NULL = legacy default).
+ *  The current CUDA device is the context's device.
+ *  Errors: ZERO_EINVAL (K != 12, stage not in 0..3, bad dtype combination,
+ *  rank/n_d/transport mismatch, layout errors), ZERO_EUNSUPPORTED (R32 with the
+ *  NCCL transport, stage 0 with R32), ZERO_ECUDA. */
+zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage, int K,
+                      const zero_config* cfg, zero_transport transport, void* nccl_comm,
+                      void* compute_stream, struct zero_ctx** out);
+
+/* Bytes of each arena the caller must allocate (device memory, >= 256-B aligned).
+ *  opt     12 * S_e : fp32 master | momentum | variance, S_e elements each
+ *                     (S_e = Psi'/N_d; Psi' at stage 0)            -- K Psi / N_d
+ *  p16     2 * Psi' (stages 0-2: full replica) or 2 * Psi'/N_d (stage 3 shard)
+ *  grad    2 * Psi' (stages 0/1: flat gradient buffer, reduced in place) or
+ *          pool_buckets * max B_k * 2 (stages 2/3 staging pool, N_d > 1); 0 otherwise
+ *  gred    reduced-gradient shard: stages 2/3 R16 2*Psi'/N_d, R32 4*Psi'/N_d;
+ *          stage 1 R32 4*Psi'/N_d; 0 otherwise
+ *  gather  stage 3, N_d > 1: (prefetch_depth + 1) * max layer elements * 2
+ *  scratch device state, norm slots, partial sums, segment table (< 1 MB)
+ * The grad/gred/gather/scratch arenas are the only transient buffers: nothing is
+ * allocated during a step (M_D). */
+typedef struct {
+  uint64_t opt_bytes, p16_bytes, grad_bytes, gred_bytes, gather_bytes, scratch_bytes;
+} zero_sizes;
+zero_status zero_buffer_sizes(const struct zero_ctx* ctx, zero_sizes* out);
+
+typedef struct {
+  void *opt, *p16, *grad, *gred, *gather, *scratch;   /* device pointers, caller-owned */
+} zero_buffers;
+/* Bind the caller's arenas (NULL allowed where the size is 0) and zero them on the
+ * compute stream.  The library never frees them. */
+zero_status zero_bind_buffers(struct zero_ctx* ctx, const zero_buffers* bufs);
+
+/* Link n contexts of one process and one device into a PEER group (BASELINE config
+ * 1: N_d simulated ranks on one GPU).  ranks[r] must have rank r, transport PEER,
+ * the same layout/stage/config/stream, and bound buffers.  The pull reduce-scatter
+ * of bucket k is issued when the last rank has flattened k; zero_step of any rank
+ * may run once every rank reduced every bucket of the step. */
+zero_status zero_sim_group(struct zero_ctx* const* ranks, int n);
+
+/* Initialise the model states from the full fp32 master weights: tensor_master[t]
+ * is a device pointer to tensor t's numel fp32 values (every rank passes the same
+ * values).  Writes this rank's fp32 shard, zeroes m and v, t = 0, and writes the
+ * 16-bit parameters (full replica at stages 0-2, own shard at stage 3).
+ * Pointers are borrowed until the call's stream work completes. */
+zero_status zero_load_master(struct zero_ctx* ctx, const void* const* tensor_master);
+
+/* Register per-tensor gradient pointers (device; dtype = grad_dtype; tensor t has
+ * numel contiguous elements).  Used by zero_reduce_grads when it is passed NULL. */
+zero_status zero_set_grad_ptrs(struct zero_ctx* ctx, const void* const* tensor_grads);
+
+/* Bucket k's gradients are complete (backward hook, buckets in any order):
+ * flatten/cast/prescale them into the bucket (M_D copy; "fuse all the
+ * gradients into a single flattened buffer"), then reduce-scatter the bucket
+ * so this rank holds the sum of its slice ("perform reduction on the entire
+ * bucket at once") and the slice's overflow flag and norm partial.
+ * tensor_grads: NULL (registered pointers) or an array of n_tensors device pointers.
+ * Errors: ZERO_EINVAL (bad k, missing pointer), ZERO_ESTATE (k already reduced this step). */
+zero_status zero_reduce_grads(struct zero_ctx* ctx, uint32_t bucket, const void* const* tensor_grads);
+
+/* Finish the step: global overflow decision and grad norm (all-reduced), loss-scale
+ * update, fused Adam on the owned shard writing the recast 16-bit parameters into
+ * the all-gather buffer, then the all-gather (stages 1/2, "all-gather ... at
+ * the end of each training step"; stage 0 updates everything locally; stage 3
+ * keeps only the shard).  host_out (optional, pinned host memory for
+ * asynchrony) receives the step record when the step's work completes.
+ * Errors: ZERO_ESTATE if some bucket of the step was not reduced. */
+zero_status zero_step(struct zero_ctx* ctx, zero_step_info* host_out);
+
+/* Stage 3: make layer `layer`'s 16-bit parameters available (all-gather of its
+ * buckets into a pool slot, "spread ... across the entire forward
+ * propagation ... once again for the backward propagation in the reverse order")
+ * and prefetch the next prefetch_depth layers in the current direction (ascending
+ * after an ascending call, descending otherwise).  views_out (host array of
+ * n_tensors entries, may be NULL) receives device pointers for the layer's tensors
+ * (others untouched); valid until zero_release_params(layer).  The caller's stream
+ * is ordered after the gather.  Errors: ZERO_ESTATE at stages 0-2 or when the pool
+ * is exhausted by unreleased layers; ZERO_EINVAL for an unknown layer. */
+zero_status zero_gather_params(struct zero_ctx* ctx, uint32_t layer, void** views_out);
+zero_status zero_release_params(struct zero_ctx* ctx, uint32_t layer);
+
+/* Stages 0-2: device pointer of tensor t's 16-bit parameters in the replica. */
+zero_status zero_param_view(const struct zero_ctx* ctx, uint32_t tensor, void** p16);
+
+/* Synchronous queries (they synchronize the compute stream when device data is read). */
+enum {
+  ZERO_Q_LAYOUT = 0,      /* out: zero_layout_info */
+  ZERO_Q_MEMORY = 1,      /* out: zero_memory */
+  ZERO_Q_COMM = 2,        /* out: zero_comm_counters */
+  ZERO_Q_STEP = 3,        /* out: zero_step_info of the last step (synchronizes) */
+  ZERO_Q_BUCKETS = 4,     /* out: zero_bucket[n_buckets] */
+  ZERO_Q_PIECES = 5,      /* out: zero_piece[n_pieces] */
+  ZERO_Q_STATE = 6,       /* out: zero_device_state (synchronizes) */
+  ZERO_Q_TIMING = 7       /* out: zero_timing, accumulated since the last TIMING query
+                             (synchronizes; needs cfg.timing = 1), then reset */
+};
+typedef struct {          /* persistent model-state bytes on this rank (Fig. 1 categories) */
+  uint64_t params16, grads16, optimizer, reduced_grad_extra, staging, gather_pool, scratch;
+} zero_memory;
+typedef struct {          /* elements this rank sent, cumulative (S:173 CommStats) */
+  uint64_t reduce_scatter, all_gather, all_reduce, steps;
+} zero_comm_counters;
+typedef struct {          /* loss-scale / Adam scalars (reading c-4) */
+  double b1t, b2t;
+  uint64_t t;
+  float loss_scale;
+  uint32_t good_steps;
+} zero_device_state;
+typedef struct {          /* device time per phase, CUDA events on the launching stream */
+  double reduce_ms;       /* first flatten of a step -> last reduce-scatter/epilogue issued */
+  double adam_ms;         /* the fused Adam kernel (sum over steps) */
+  double step_ms;         /* zero_step: decision + Adam + all-gather */
+  uint64_t steps;         /* steps accumulated */
+  uint64_t kernel_launches;  /* library kernels launched (all, cumulative, never reset) */
+  uint64_t adam_launches;
+} zero_timing;
+zero_status zero_query(const struct zero_ctx* ctx, int what, void* out, size_t out_bytes);
+
+/* Last error text of ctx (NULL: of the calling thread's last failed zero_init). */
+const char* zero_last_error(const struct zero_ctx* ctx);
+void zero_destroy(struct zero_ctx* ctx);
+
+/* Pure host functions (no GPU): the closed forms the runtime reports against. */
+/* Fig. 1 / Table 1: per-device model-state bytes for stage 0..3 (floor). */
+uint64_t zero_model_state_bytes(uint64_t psi, int K, int n_d, int stage);
+/* Elements each rank sends per step: 2 Psi'(N-1)/N (stages 0-2), 3 Psi'(N-1)/N (stage 3). */
+uint64_t zero_comm_elems_per_rank(uint64_t psi_padded, int n_d, int stage);
+int zero_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZERO_B200_H */

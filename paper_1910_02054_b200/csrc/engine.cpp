@@ -1,0 +1,1224 @@
+// Host engine of the ZeRO-DP hot path: layout, arenas, stage schedule, stream/event
+// plan and the C ABI declared in include/zero_b200.h.  Citations "P:n" are lines of
+// the paper; "c-k" are the readings in DESIGN.md §3.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "zero_b200.h"
+#include "zero_internal.h"
+
+using namespace zero;
+
+namespace {
+
+thread_local std::string g_init_error;
+
+int to_dt(zero_dtype d) { return d == ZERO_FP16 ? DT_F16 : d == ZERO_BF16 ? DT_BF16 : DT_F32; }
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+// ---------------------------------------------------------------------------
+// Layout (reading c-7): written from the rule in DESIGN.md §3, independently of the
+// oracle.  Q = N*A, cap = floor(C_B/Q)*Q; a bucket never spans layers; a tensor that
+// does not fit at the next A-aligned position is split at cap; buckets padded to Q.
+// ---------------------------------------------------------------------------
+struct LayoutResult {
+  std::vector<zero_bucket> buckets;
+  std::vector<zero_piece> pieces;
+  zero_layout_info info{};
+  std::string error;
+};
+
+bool plan(const zero_layout_desc* d, int n_d, LayoutResult& out) {
+  if (!d || (d->n_tensors > 0 && !d->tensors)) { out.error = "null layout descriptor"; return false; }
+  if (n_d < 1 || n_d > ZERO_MAX_RANKS) { out.error = "n_d out of range 1..8"; return false; }
+  const uint64_t A = d->align_elems;
+  if (A == 0 || (A & (A - 1))) { out.error = "align_elems must be a power of two"; return false; }
+  const uint64_t Q = (uint64_t)n_d * A;
+  uint64_t cap = 0;  // 0 = unlimited
+  if (d->bucket_cap_elems) {
+    if (d->bucket_cap_elems < Q) { out.error = "bucket_cap_elems < N_d * align_elems"; return false; }
+    cap = d->bucket_cap_elems / Q * Q;
+  }
+  for (uint32_t t = 1; t < d->n_tensors; ++t)
+    if (d->tensors[t].layer < d->tensors[t - 1].layer) { out.error = "layer ids must be non-decreasing"; return false; }
+
+  struct Cur { uint32_t layer; uint64_t used; std::vector<zero_piece> p; } cur{0, 0, {}};
+  bool have_layer = false;
+  std::vector<Cur> closed;
+  auto close = [&](uint32_t next_layer) {
+    if (cur.used > 0) closed.push_back(cur);
+    cur = Cur{next_layer, 0, {}};
+  };
+  uint64_t psi = 0;
+  for (uint32_t t = 0; t < d->n_tensors; ++t) {
+    const uint64_t n = d->tensors[t].numel;
+    const uint32_t L = d->tensors[t].layer;
+    if (n == 0) continue;
+    psi += n;
+    if (!have_layer) { cur.layer = L; have_layer = true; }
+    if (cur.used > 0 && L != cur.layer) close(L);
+    if (cur.used == 0) cur.layer = L;
+    uint64_t rem = n, toff = 0;
+    while (rem > 0) {
+      const uint64_t start = align_up(cur.used, A);
+      if (cap && start >= cap) { close(L); continue; }
+      const uint64_t room = cap ? cap - start : rem;
+      const uint64_t take = std::min(rem, room);
+      cur.p.push_back(zero_piece{t, 0, toff, start, take});
+      cur.used = start + take;
+      rem -= take;
+      toff += take;
+      if (rem > 0) close(L);
+    }
+  }
+  close(0);
+  if (psi == 0) { out.error = "layout has no elements"; return false; }
+
+  uint64_t base = 0, shard_off = 0, maxb = 0;
+  std::map<uint32_t, int> layers;
+  for (size_t k = 0; k < closed.size(); ++k) {
+    zero_bucket b{};
+    b.layer = closed[k].layer;
+    b.size = align_up(closed[k].used, Q);
+    b.base = base;
+    b.shard_off = shard_off;
+    b.first_piece = (uint32_t)out.pieces.size();
+    b.n_pieces = (uint32_t)closed[k].p.size();
+    for (auto p : closed[k].p) { p.bucket = (uint32_t)k; out.pieces.push_back(p); }
+    out.buckets.push_back(b);
+    base += b.size;
+    shard_off += b.size / n_d;
+    maxb = std::max(maxb, b.size);
+    layers[b.layer] = 1;
+  }
+  out.info.psi = psi;
+  out.info.psi_padded = base;
+  out.info.shard = base / n_d;
+  out.info.n_buckets = (uint32_t)out.buckets.size();
+  out.info.n_pieces = (uint32_t)out.pieces.size();
+  out.info.n_layers = (uint32_t)layers.size();
+  out.info.max_bucket = maxb > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)maxb;
+  return true;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+struct ZeroGroup;
+
+#define CK0(expr)                                                                             \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) return c->fail(ZERO_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+struct LayerInfo {
+  uint32_t layer;
+  uint32_t k0, k1;          // buckets [k0, k1)
+  uint64_t flat0, flat1;    // global flat range
+};
+
+struct GatherSlot {
+  int layer = -1;           // layer held (-1 free)
+  bool released = true;
+  cudaEvent_t ready = nullptr, freed = nullptr;
+  uint64_t lru = 0;
+};
+
+struct zero_ctx {
+  // configuration
+  int n_d = 1, rank = 0, stage = 1;
+  zero_config cfg{};
+  zero_transport transport = ZERO_TRANSPORT_LOCAL;
+  ncclComm_t comm = nullptr;
+  cudaStream_t stream = nullptr;       // caller's compute stream
+  cudaStream_t comm_stream = nullptr;  // library stream for NCCL work
+  bool own_comm_stream = false;
+  int pdt = DT_BF16, gdt = DT_BF16;
+  bool r32 = false;                    // reduced gradient kept in fp32 (R32 and N_d > 1)
+
+  // layout
+  std::vector<zero_tensor> tensors;
+  std::vector<zero_bucket> buckets;
+  std::vector<zero_piece> pieces;
+  zero_layout_info info{};
+  std::vector<LayerInfo> layers;
+  std::map<uint32_t, int> layer_index;
+  std::vector<std::vector<FlatPiece>> flat_tmpl;   // per bucket: data + zero pieces (src = tensor id)
+  std::vector<std::vector<uint32_t>> flat_tensor;  // per bucket: tensor id per flat piece (UINT32_MAX = zero)
+  std::vector<int> slot_base;                      // per bucket: first epilogue slot
+  int n_slots = 0;
+  std::vector<uint64_t> tensor_flat;               // tensor -> global flat offset of element 0
+  uint64_t S_e = 0;                                // elements this rank updates
+  uint64_t max_layer = 0;
+  uint32_t pool = 2;
+
+  // arenas
+  zero_sizes sizes{};
+  zero_buffers bufs{};
+  bool bound = false;
+  float *p32 = nullptr, *m = nullptr, *v = nullptr;
+  uint16_t* p16 = nullptr;
+  uint16_t* grad = nullptr;
+  void* gred = nullptr;
+  uint16_t* gather = nullptr;
+  DevState* st = nullptr;
+  Slot* slots = nullptr;
+  GridPartials* part_compute = nullptr;
+  GridPartials* part_comm = nullptr;
+  RankPartial* my_partial = nullptr;
+  RankPartial* gathered = nullptr;
+  AdamSeg* segs = nullptr;
+  std::vector<AdamSeg> segs_host;
+  int sms = 148;
+
+  // per-step tracking
+  std::vector<uint8_t> reduced;
+  uint32_t n_reduced = 0;
+  std::vector<int> pool_pending;                   // per pool slot: bucket awaiting its RS (-1 none)
+  std::vector<const void*> grad_ptrs;
+  std::vector<cudaEvent_t> ev_pool_free;           // NCCL: RS of the slot's last bucket done
+  cudaEvent_t ev_flat = nullptr, ev_step = nullptr, ev_tmp = nullptr;
+  bool stepped_this_round = false;
+
+  // stage 3
+  std::vector<GatherSlot> gslots;
+  std::vector<int> layer_slot;                     // layer index -> gather slot (-1)
+  int last_layer = -1;
+  int direction = +1;
+  uint64_t lru_clock = 0;
+
+  ZeroGroup* group = nullptr;
+  zero_comm_counters counters{};
+
+  // phase timing (cfg.timing): one event set per step, reused from a pool
+  struct StepEvents { cudaEvent_t r0 = nullptr, r1 = nullptr, a0 = nullptr, a1 = nullptr, s1 = nullptr; };
+  std::vector<StepEvents> ev_pool;
+  size_t ev_used = 0;
+  bool step_open = false;          // a reduce phase began (r0 recorded)
+  uint64_t launches = 0, adam_launches = 0;
+  zero_status timing_events(StepEvents** out);
+
+  zero_status sticky = ZERO_OK;
+  std::string err;
+
+  zero_status fail(zero_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    err = buf;
+    if (s == ZERO_ECUDA || s == ZERO_ENCCL) sticky = s;
+    return s;
+  }
+
+  // destinations ------------------------------------------------------------
+  uint64_t slice(uint32_t k) const { return buckets[k].size / n_d; }
+  uint16_t* flat_dst(uint32_t k) const {       // where bucket k is flattened
+    const zero_bucket& b = buckets[k];
+    if (stage <= 1) return grad + b.base;
+    if (n_d == 1) return reinterpret_cast<uint16_t*>(gred) + b.shard_off;
+    return grad + (uint64_t)(k % pool) * maxB;
+  }
+  // where bucket k's reduced slice (this rank's) lives
+  void* rs_dst(uint32_t k) const {
+    const zero_bucket& b = buckets[k];
+    if (r32) return reinterpret_cast<float*>(gred) + b.shard_off;
+    if (stage <= 1) return grad + b.base + (uint64_t)rank * slice(k);
+    return reinterpret_cast<uint16_t*>(gred) + b.shard_off;
+  }
+  uint64_t maxB = 0;
+};
+
+zero_status zero_ctx::timing_events(StepEvents** out) {
+  zero_ctx* c = this;
+  if (ev_used == ev_pool.size()) {
+    StepEvents e;
+    CK0(cudaEventCreate(&e.r0));
+    CK0(cudaEventCreate(&e.r1));
+    CK0(cudaEventCreate(&e.a0));
+    CK0(cudaEventCreate(&e.a1));
+    CK0(cudaEventCreate(&e.s1));
+    ev_pool.push_back(e);
+  }
+  *out = &ev_pool[ev_used];
+  return ZERO_OK;
+}
+
+// A PEER group of contexts sharing one device and one stream (config 1's simulated
+// ranks).  Collective steps are issued once every member reached them.
+struct ZeroGroup {
+  int n = 0;
+  zero_ctx* ranks[ZERO_MAX_RANKS] = {};
+  std::vector<int> flat_count;   // per bucket: ranks that flattened it this step
+  uint32_t reduced_buckets = 0;  // buckets whose pull reduce-scatter was issued
+  int stepped = 0;               // ranks that ran zero_step this round
+};
+
+namespace {
+
+#define CK(expr)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) return c->fail(ZERO_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+#define NK(expr)                                                                              \
+  do {                                                                                        \
+    ncclResult_t r_ = (expr);                                                                 \
+    if (r_ != ncclSuccess) return c->fail(ZERO_ENCCL, "%s: %s", #expr, ncclGetErrorString(r_)); \
+  } while (0)
+#define STICKY(c)                                  \
+  do {                                             \
+    if (!(c)) return ZERO_EINVAL;                  \
+    if ((c)->sticky != ZERO_OK) return (c)->sticky; \
+  } while (0)
+
+ncclDataType_t nccl_dt(int dt) { return dt == DT_F16 ? ncclFloat16 : dt == DT_BF16 ? ncclBfloat16 : ncclFloat32; }
+
+int grid_for(uint64_t work_items, int per_sm, int sms) {
+  const uint64_t cap = (uint64_t)per_sm * sms;
+  uint64_t g = work_items < cap ? work_items : cap;
+  if (g < 1) g = 1;
+  if (g > (uint64_t)kMaxGrid) g = kMaxGrid;
+  return (int)g;
+}
+
+// bytes of the scratch arena and the offsets inside it
+struct ScratchLayout {
+  size_t st, slots, part_compute, part_comm, my_partial, gathered, segs, total;
+};
+ScratchLayout scratch_layout(int n_slots, size_t n_segs) {
+  ScratchLayout s{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+  s.st = take(sizeof(DevState));
+  s.slots = take(sizeof(Slot) * (size_t)std::max(n_slots, 1));
+  s.part_compute = take(sizeof(GridPartials));
+  s.part_comm = take(sizeof(GridPartials));
+  s.my_partial = take(sizeof(RankPartial));
+  s.gathered = take(sizeof(RankPartial) * ZERO_MAX_RANKS);
+  s.segs = take(sizeof(AdamSeg) * std::max<size_t>(n_segs, 1));
+  s.total = o;
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+int zero_abi_version(void) { return ZERO_ABI_VERSION; }
+
+zero_status zero_plan_layout(const zero_layout_desc* desc, int n_d, zero_layout_info* info, zero_bucket* buckets,
+                             uint32_t cap_buckets, zero_piece* pieces, uint32_t cap_pieces) {
+  LayoutResult r;
+  if (!plan(desc, n_d, r)) { g_init_error = r.error; return ZERO_EINVAL; }
+  if (info) *info = r.info;
+  if (buckets) {
+    if (cap_buckets < r.info.n_buckets) return ZERO_EINVAL;
+    std::memcpy(buckets, r.buckets.data(), sizeof(zero_bucket) * r.buckets.size());
+  }
+  if (pieces) {
+    if (cap_pieces < r.info.n_pieces) return ZERO_EINVAL;
+    std::memcpy(pieces, r.pieces.data(), sizeof(zero_piece) * r.pieces.size());
+  }
+  return ZERO_OK;
+}
+
+uint64_t zero_model_state_bytes(uint64_t psi, int K, int n_d, int stage) {
+  // Fig. 1 / P:360, P:369, P:397 -- exact in 128-bit, floored.
+  using u128 = unsigned __int128;
+  if (n_d < 1) return 0;
+  const u128 p = psi, k = (u128)K, n = (u128)n_d;
+  switch (stage) {
+    case 0: return (uint64_t)((4 + k) * p);
+    case 1: return (uint64_t)((4 * p * n + k * p) / n);
+    case 2: return (uint64_t)((2 * p * n + (2 + k) * p) / n);
+    case 3: return (uint64_t)(((4 + k) * p) / n);
+    default: return 0;
+  }
+}
+
+uint64_t zero_comm_elems_per_rank(uint64_t psi_padded, int n_d, int stage) {
+  // P:445, P:473 (2 Psi) and P:476-478 (3 Psi) with the exact ring factor (N-1)/N.
+  if (n_d < 1) return 0;
+  const uint64_t one = psi_padded / (uint64_t)n_d * (uint64_t)(n_d - 1);
+  return stage == 3 ? 3 * one : 2 * one;
+}
+
+zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage, int K, const zero_config* cfg,
+                      zero_transport transport, void* nccl_comm, void* compute_stream, zero_ctx** out) {
+  g_init_error.clear();
+  auto bad = [&](const char* why) { g_init_error = why; return ZERO_EINVAL; };
+  if (!out || !cfg) return bad("null argument");
+  *out = nullptr;
+  if (K != 12) return bad("K must be 12 (mixed-precision Adam, P:266)");
+  if (stage < 0 || stage > 3) return bad("stage must be 0..3");
+  if (n_d < 1 || n_d > ZERO_MAX_RANKS || rank < 0 || rank >= n_d) return bad("rank/n_d out of range");
+  if (cfg->param_dtype != ZERO_FP16 && cfg->param_dtype != ZERO_BF16) return bad("param_dtype must be FP16 or BF16");
+  if (cfg->grad_dtype != cfg->param_dtype && cfg->grad_dtype != ZERO_FP32) return bad("grad_dtype must equal param_dtype or be FP32");
+  if (cfg->reduce_mode != ZERO_R16 && cfg->reduce_mode != ZERO_R32) return bad("reduce_mode");
+  if (!(cfg->lr > 0.f) || !(cfg->beta1 >= 0.f && cfg->beta1 < 1.f) || !(cfg->beta2 >= 0.f && cfg->beta2 < 1.f) ||
+      !(cfg->eps > 0.f))
+    return bad("Adam hyper-parameters out of range");
+  if (!(cfg->loss_scale > 0.f) || !(cfg->grad_prescale > 0.f)) return bad("loss_scale and grad_prescale must be > 0");
+  if (cfg->dynamic_loss_scale && (cfg->scale_window == 0 || !(cfg->min_loss_scale > 0.f)))
+    return bad("dynamic loss scaling needs scale_window > 0 and min_loss_scale > 0");
+  if (transport == ZERO_TRANSPORT_LOCAL && n_d != 1) return bad("LOCAL transport requires n_d == 1");
+  if (transport == ZERO_TRANSPORT_NCCL && n_d > 1 && !nccl_comm) return bad("NCCL transport requires a communicator");
+  if (transport != ZERO_TRANSPORT_LOCAL && transport != ZERO_TRANSPORT_NCCL && transport != ZERO_TRANSPORT_PEER)
+    return bad("unknown transport");
+  const bool r32 = cfg->reduce_mode == ZERO_R32 && n_d > 1;
+  if (r32 && transport == ZERO_TRANSPORT_NCCL) { g_init_error = "R32 is implemented on the PEER transport only"; return ZERO_EUNSUPPORTED; }
+  if (r32 && stage == 0) { g_init_error = "stage 0 supports R16 only"; return ZERO_EUNSUPPORTED; }
+
+  LayoutResult L;
+  if (!plan(desc, n_d, L)) return bad(L.error.c_str());
+
+  zero_ctx* c = new zero_ctx();
+  c->n_d = n_d;
+  c->rank = rank;
+  c->stage = stage;
+  c->cfg = *cfg;
+  if (c->cfg.prefetch_depth == 0) c->cfg.prefetch_depth = 1;
+  c->pool = c->cfg.pool_buckets ? c->cfg.pool_buckets : 2;
+  c->transport = (n_d == 1) ? ZERO_TRANSPORT_LOCAL : transport;
+  c->comm = reinterpret_cast<ncclComm_t>(nccl_comm);
+  c->stream = reinterpret_cast<cudaStream_t>(compute_stream);
+  c->pdt = to_dt(cfg->param_dtype);
+  c->gdt = to_dt(cfg->grad_dtype);
+  c->r32 = r32;
+  c->tensors.assign(desc->tensors, desc->tensors + desc->n_tensors);
+  c->buckets = L.buckets;
+  c->pieces = L.pieces;
+  c->info = L.info;
+  for (auto& b : c->buckets) c->maxB = std::max(c->maxB, b.size);
+
+  // tensor -> flat offset (split tensors are contiguous: split points are multiples of Q)
+  c->tensor_flat.assign(c->tensors.size(), UINT64_MAX);
+  for (auto& p : c->pieces)
+    if (p.tensor_off == 0) c->tensor_flat[p.tensor] = c->buckets[p.bucket].base + p.bucket_off;
+
+  // layers
+  for (uint32_t k = 0; k < c->info.n_buckets; ++k) {
+    const zero_bucket& b = c->buckets[k];
+    auto it = c->layer_index.find(b.layer);
+    if (it == c->layer_index.end()) {
+      c->layer_index[b.layer] = (int)c->layers.size();
+      c->layers.push_back(LayerInfo{b.layer, k, k + 1, b.base, b.base + b.size});
+    } else {
+      LayerInfo& li = c->layers[it->second];
+      li.k1 = k + 1;
+      li.flat1 = b.base + b.size;
+    }
+  }
+  for (auto& li : c->layers) c->max_layer = std::max(c->max_layer, li.flat1 - li.flat0);
+
+  // flatten templates: data pieces + zero pieces covering [0, B_k) exactly
+  c->flat_tmpl.resize(c->info.n_buckets);
+  c->flat_tensor.resize(c->info.n_buckets);
+  c->slot_base.resize(c->info.n_buckets);
+  int slots = 0;
+  for (uint32_t k = 0; k < c->info.n_buckets; ++k) {
+    const zero_bucket& b = c->buckets[k];
+    uint64_t pos = 0;
+    auto add = [&](const void* tensor_tag, uint32_t tensor, uint64_t toff, uint64_t off, uint64_t n) {
+      FlatPiece fp{};
+      fp.src = tensor_tag;
+      fp.dst_off = off;
+      fp.count = n;
+      fp.chunk_begin = toff;  // holds tensor_off until the launch fills src/chunks
+      c->flat_tmpl[k].push_back(fp);
+      c->flat_tensor[k].push_back(tensor);
+    };
+    for (uint32_t j = 0; j < b.n_pieces; ++j) {
+      const zero_piece& p = c->pieces[b.first_piece + j];
+      if (p.bucket_off > pos) add(nullptr, UINT32_MAX, 0, pos, p.bucket_off - pos);
+      add(nullptr, p.tensor, p.tensor_off, p.bucket_off, p.count);
+      pos = p.bucket_off + p.count;
+    }
+    if (pos < b.size) add(nullptr, UINT32_MAX, 0, pos, b.size - pos);
+    c->slot_base[k] = slots;
+    slots += (int)((c->flat_tmpl[k].size() + kMaxFlatPieces - 1) / kMaxFlatPieces);
+  }
+  c->n_slots = slots;
+
+  // Adam segments over this rank's local index space
+  c->S_e = stage == 0 ? c->info.psi_padded : c->info.shard;
+  for (uint32_t k = 0; k < c->info.n_buckets; ++k) {
+    const zero_bucket& b = c->buckets[k];
+    const uint64_t sl = b.size / n_d;
+    AdamSeg s{};
+    if (stage == 0) {
+      s.local_off = b.base;
+      s.count = b.size;
+      s.g_off = b.base;
+      s.p16_off = b.base;
+    } else {
+      s.local_off = b.shard_off;
+      s.count = sl;
+      const uint64_t mine = b.base + (uint64_t)rank * sl;
+      s.g_off = (stage == 1 && !r32) ? mine : b.shard_off;
+      s.p16_off = stage == 3 ? b.shard_off : mine;
+    }
+    c->segs_host.push_back(s);
+  }
+
+  // arena sizes (zero_sizes doc in the header)
+  const uint64_t P = c->info.psi_padded, S = c->info.shard;
+  zero_sizes& z = c->sizes;
+  z.opt_bytes = 12ull * c->S_e;
+  z.p16_bytes = 2ull * (stage == 3 ? S : P);
+  if (stage <= 1) z.grad_bytes = 2ull * P;
+  else z.grad_bytes = (n_d > 1) ? 2ull * c->pool * c->maxB : 0;
+  if (stage >= 2) z.gred_bytes = (r32 ? 4ull : 2ull) * S;
+  else z.gred_bytes = r32 ? 4ull * S : 0;
+  z.gather_bytes = (stage == 3 && n_d > 1) ? 2ull * (c->cfg.prefetch_depth + 1) * c->max_layer : 0;
+  z.scratch_bytes = scratch_layout(c->n_slots, c->segs_host.size()).total;
+
+  c->reduced.assign(c->info.n_buckets, 0);
+  c->pool_pending.assign(c->pool, -1);
+  c->grad_ptrs.assign(c->tensors.size(), nullptr);
+  c->layer_slot.assign(c->layers.size(), -1);
+  *out = c;
+  return ZERO_OK;
+}
+
+zero_status zero_buffer_sizes(const zero_ctx* c, zero_sizes* out) {
+  if (!c || !out) return ZERO_EINVAL;
+  *out = c->sizes;
+  return ZERO_OK;
+}
+
+zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
+  STICKY(c);
+  if (!b) return ZERO_EINVAL;
+  if (c->bound) return c->fail(ZERO_ESTATE, "buffers already bound");
+  const zero_sizes& z = c->sizes;
+  auto need = [&](const void* p, uint64_t bytes, const char* name) -> bool {
+    if (bytes == 0) return true;
+    if (!p) { c->fail(ZERO_EINVAL, "arena %s (%llu bytes) is NULL", name, (unsigned long long)bytes); return false; }
+    if (reinterpret_cast<uintptr_t>(p) & 255) { c->fail(ZERO_EINVAL, "arena %s is not 256-byte aligned", name); return false; }
+    return true;
+  };
+  if (!need(b->opt, z.opt_bytes, "opt") || !need(b->p16, z.p16_bytes, "p16") || !need(b->grad, z.grad_bytes, "grad") ||
+      !need(b->gred, z.gred_bytes, "gred") || !need(b->gather, z.gather_bytes, "gather") ||
+      !need(b->scratch, z.scratch_bytes, "scratch"))
+    return ZERO_EINVAL;
+  c->bufs = *b;
+  c->p32 = reinterpret_cast<float*>(b->opt);
+  c->m = c->p32 + c->S_e;
+  c->v = c->m + c->S_e;
+  c->p16 = reinterpret_cast<uint16_t*>(b->p16);
+  c->grad = reinterpret_cast<uint16_t*>(b->grad);
+  c->gred = b->gred;
+  c->gather = reinterpret_cast<uint16_t*>(b->gather);
+  const ScratchLayout sl = scratch_layout(c->n_slots, c->segs_host.size());
+  char* s = reinterpret_cast<char*>(b->scratch);
+  c->st = reinterpret_cast<DevState*>(s + sl.st);
+  c->slots = reinterpret_cast<Slot*>(s + sl.slots);
+  c->part_compute = reinterpret_cast<GridPartials*>(s + sl.part_compute);
+  c->part_comm = reinterpret_cast<GridPartials*>(s + sl.part_comm);
+  c->my_partial = reinterpret_cast<RankPartial*>(s + sl.my_partial);
+  c->gathered = reinterpret_cast<RankPartial*>(s + sl.gathered);
+  c->segs = reinterpret_cast<AdamSeg*>(s + sl.segs);
+  c->sms = sm_count();
+
+  // streams and events
+  if (c->transport == ZERO_TRANSPORT_NCCL) {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
+    c->own_comm_stream = true;
+    c->ev_pool_free.assign(c->pool, nullptr);
+    for (auto& e : c->ev_pool_free) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  } else {
+    c->comm_stream = c->stream;
+  }
+  CK(cudaEventCreateWithFlags(&c->ev_flat, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_step, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_tmp, cudaEventDisableTiming));
+  if (c->stage == 3) {
+    c->gslots.resize(c->cfg.prefetch_depth + 1);
+    for (auto& g : c->gslots) {
+      CK(cudaEventCreateWithFlags(&g.ready, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&g.freed, cudaEventDisableTiming));
+    }
+  }
+
+  // zero every arena (padding must hold 0, c-7), upload the segment table, init state
+  const void* ptrs[6] = {b->opt, b->p16, b->grad, b->gred, b->gather, b->scratch};
+  const uint64_t sz[6] = {z.opt_bytes, z.p16_bytes, z.grad_bytes, z.gred_bytes, z.gather_bytes, z.scratch_bytes};
+  for (int i = 0; i < 6; ++i)
+    if (sz[i]) CK(cudaMemsetAsync(const_cast<void*>(ptrs[i]), 0, sz[i], c->stream));
+  CK(cudaMemcpyAsync(c->segs, c->segs_host.data(), sizeof(AdamSeg) * c->segs_host.size(), cudaMemcpyHostToDevice,
+                     c->stream));
+  const float inv = (float)(1.0 / ((double)c->n_d * (double)c->cfg.loss_scale * (double)c->cfg.grad_prescale));
+  CK(launch_init_state(c->st, c->cfg.loss_scale, inv, c->stream));
+  c->launches++;
+  // the segment table is read from host memory by the async copy: wait for it
+  CK(cudaStreamSynchronize(c->stream));
+  c->bound = true;
+  return ZERO_OK;
+}
+
+zero_status zero_load_master(zero_ctx* c, const void* const* tensor_master) {
+  STICKY(c);
+  if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
+  if (!tensor_master) return c->fail(ZERO_EINVAL, "tensor_master is NULL");
+  for (auto& p : c->pieces)
+    if (!tensor_master[p.tensor]) return c->fail(ZERO_EINVAL, "master pointer of tensor %u is NULL", p.tensor);
+  CK(cudaMemsetAsync(c->m, 0, 8ull * c->S_e, c->stream));  // m and v are contiguous
+  for (uint32_t k = 0; k < c->info.n_buckets; ++k) {
+    const zero_bucket& b = c->buckets[k];
+    const uint64_t sl = b.size / c->n_d;
+    for (uint32_t j = 0; j < b.n_pieces; ++j) {
+      const zero_piece& p = c->pieces[b.first_piece + j];
+      LoadArgs a{};
+      a.src = reinterpret_cast<const float*>(tensor_master[p.tensor]) + p.tensor_off;
+      a.count = p.count;
+      a.flat_off = b.base + p.bucket_off;
+      if (c->stage == 0) {
+        a.own_lo = b.base;
+        a.own_hi = b.base + b.size;
+        a.local_base = b.base;
+      } else {
+        a.own_lo = b.base + (uint64_t)c->rank * sl;
+        a.own_hi = a.own_lo + sl;
+        a.local_base = b.shard_off;
+      }
+      a.p32 = c->p32;
+      a.p16 = c->p16;
+      a.p16_mode = c->stage == 3 ? 1 : 0;
+      a.p_dtype = c->pdt;
+      CK(launch_load(a, c->stream));
+      c->launches++;
+    }
+  }
+  const float inv = (float)(1.0 / ((double)c->n_d * (double)c->cfg.loss_scale * (double)c->cfg.grad_prescale));
+  CK(launch_init_state(c->st, c->cfg.loss_scale, inv, c->stream));
+  c->launches++;
+  return ZERO_OK;
+}
+
+zero_status zero_set_grad_ptrs(zero_ctx* c, const void* const* g) {
+  STICKY(c);
+  if (!g) return c->fail(ZERO_EINVAL, "null pointer array");
+  c->grad_ptrs.assign(g, g + c->tensors.size());
+  return ZERO_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// issue the flatten of bucket k (compute stream).  epilogue at N_d == 1.
+zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads) {
+  const auto& tmpl = c->flat_tmpl[k];
+  uint16_t* dst = c->flat_dst(k);
+  const int ebytes = c->gdt == DT_F32 ? 4 : 2;
+  const bool epi = c->n_d == 1;
+  int slot = c->slot_base[k];
+  for (size_t b0 = 0; b0 < tmpl.size(); b0 += kMaxFlatPieces, ++slot) {
+    FlatArgs a{};
+    const size_t b1 = std::min(tmpl.size(), b0 + kMaxFlatPieces);
+    uint64_t chunks = 0;
+    for (size_t j = b0; j < b1; ++j) {
+      FlatPiece fp = tmpl[j];
+      const uint32_t t = c->flat_tensor[k][j];
+      if (t != UINT32_MAX) {
+        const char* base = reinterpret_cast<const char*>(grads[t]);
+        if (!base) return c->fail(ZERO_EINVAL, "gradient pointer of tensor %u is NULL", t);
+        fp.src = base + fp.chunk_begin * ebytes;  // chunk_begin held tensor_off
+      } else {
+        fp.src = nullptr;
+      }
+      fp.chunk_begin = chunks;
+      chunks += (fp.count + 4095) / 4096;
+      a.pieces[j - b0] = fp;
+    }
+    a.n_pieces = (int)(b1 - b0);
+    a.src_dtype = c->gdt;
+    a.dst_dtype = c->pdt;
+    a.epilogue = epi ? 1 : 0;
+    a.total_chunks = chunks;
+    a.dst = dst;
+    a.sigma = c->cfg.grad_prescale;
+    a.st = c->st;
+    a.part = c->part_compute;
+    a.slot = c->slots + slot;
+    CK(launch_flatten(a, grid_for(chunks, 4, c->sms), c->stream));
+    c->launches++;
+  }
+  return ZERO_OK;
+}
+
+// pull reduce-scatter of bucket k for rank c (PEER), sources = every member's flattened bucket
+zero_status issue_pull_rs(zero_ctx* c, ZeroGroup* g, uint32_t k) {
+  const uint64_t sl = c->slice(k);
+  RSArgs a{};
+  for (int j = 0; j < g->n; ++j) a.src[j] = g->ranks[j]->flat_dst(k) + (uint64_t)c->rank * sl;
+  a.dst = c->rs_dst(k);
+  a.count = sl;
+  a.n = g->n;
+  a.dtype = c->pdt;
+  a.r32 = c->r32 ? 1 : 0;
+  a.reduce = 1;
+  a.st = c->st;
+  a.part = c->part_comm;
+  a.slot = c->slots + c->slot_base[k];
+  CK(launch_reduce_scatter(a, grid_for((sl + 2047) / 2048, 4, c->sms), c->comm_stream));
+  c->launches++;
+  c->counters.reduce_scatter += sl * (uint64_t)(c->n_d - 1);
+  return ZERO_OK;
+}
+
+zero_status finish_bucket_local(zero_ctx* c, uint32_t k) {
+  c->reduced[k] = 1;
+  c->n_reduced++;
+  return ZERO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor_grads) {
+  STICKY(c);
+  if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
+  if (k >= c->info.n_buckets) return c->fail(ZERO_EINVAL, "bucket %u out of range", k);
+  if (c->reduced[k]) return c->fail(ZERO_ESTATE, "bucket %u already reduced this step", k);
+  if (c->transport == ZERO_TRANSPORT_PEER && !c->group) return c->fail(ZERO_ESTATE, "PEER context not in a group");
+  const void* const* grads = tensor_grads ? tensor_grads : c->grad_ptrs.data();
+
+  // C_B pool slot reuse (stages 2/3, N_d > 1)
+  const bool pooled = c->stage >= 2 && c->n_d > 1;
+  const uint32_t ps = pooled ? k % c->pool : 0;
+  if (pooled && c->transport == ZERO_TRANSPORT_PEER) {
+    const int pend = c->pool_pending[ps];
+    if (pend >= 0 && c->group->flat_count[pend] < c->group->n)
+      return c->fail(ZERO_ESTATE, "pool slot %u still holds bucket %d awaiting its reduce-scatter", ps, pend);
+  }
+  if (pooled && c->transport == ZERO_TRANSPORT_NCCL) CK(cudaStreamWaitEvent(c->stream, c->ev_pool_free[ps], 0));
+
+  if (c->cfg.timing && !c->step_open && c->ev_used < 4096) {
+    zero_ctx::StepEvents* ev;
+    zero_status es = c->timing_events(&ev);
+    if (es != ZERO_OK) return es;
+    CK(cudaEventRecord(ev->r0, c->stream));
+    c->step_open = true;
+  }
+  zero_status s = issue_flatten(c, k, grads);
+  if (s != ZERO_OK) return s;
+
+  if (c->n_d == 1) return finish_bucket_local(c, k);
+
+  if (c->transport == ZERO_TRANSPORT_PEER) {
+    ZeroGroup* g = c->group;
+    if (pooled) c->pool_pending[ps] = (int)k;
+    c->reduced[k] = 1;  // this rank's part is done; the collective completes below
+    if (++g->flat_count[k] == g->n) {
+      for (int j = 0; j < g->n; ++j) {
+        zero_status r = issue_pull_rs(g->ranks[j], g, k);
+        if (r != ZERO_OK) return r;
+      }
+      if (c->stage == 0) {  // all-reduce = RS + AG of the reduced slices
+        for (int j = 0; j < g->n; ++j) {
+          zero_ctx* cj = g->ranks[j];
+          CopyArgs a{};
+          const uint64_t sl = cj->slice(k);
+          for (int i = 0; i < g->n; ++i) {
+            a.src[i] = g->ranks[i]->grad + cj->buckets[k].base + (uint64_t)i * sl;
+            a.dst[i] = cj->grad + cj->buckets[k].base + (uint64_t)i * sl;
+          }
+          a.count = sl;
+          a.n = g->n;
+          zero_ctx* cc = cj;
+          if (launch_copy(a, grid_for((sl + 2047) / 2048, 2, cc->sms), cc->comm_stream) != cudaSuccess)
+            return cc->fail(ZERO_ECUDA, "pull all-gather launch failed");
+          cc->launches++;
+          cj->counters.all_gather += sl * (uint64_t)(g->n - 1);
+        }
+      }
+      for (int j = 0; j < g->n; ++j) g->ranks[j]->n_reduced++;
+      if (++g->reduced_buckets == c->info.n_buckets) {
+        for (int j = 0; j < g->n; ++j) {
+          zero_ctx* cj = g->ranks[j];
+          if (launch_decide_local(cj->slots, cj->n_slots, cj->my_partial, cj->comm_stream) != cudaSuccess)
+            return cj->fail(ZERO_ECUDA, "decide_local launch failed");
+          cj->launches++;
+        }
+      }
+    }
+    return ZERO_OK;
+  }
+
+  // NCCL: the compute stream produced the bucket; the comm stream reduces it
+  CK(cudaEventRecord(c->ev_flat, c->stream));
+  CK(cudaStreamWaitEvent(c->comm_stream, c->ev_flat, 0));
+  const zero_bucket& b = c->buckets[k];
+  const uint64_t sl = c->slice(k);
+  const ncclDataType_t dt = nccl_dt(c->pdt);
+  if (c->stage == 0) {
+    NK(ncclAllReduce(c->grad + b.base, c->grad + b.base, b.size, dt, ncclSum, c->comm, c->comm_stream));
+    c->counters.all_reduce += 2 * sl * (uint64_t)(c->n_d - 1);
+  } else {
+    NK(ncclReduceScatter(c->flat_dst(k), c->rs_dst(k), sl, dt, ncclSum, c->comm, c->comm_stream));
+    c->counters.reduce_scatter += sl * (uint64_t)(c->n_d - 1);
+  }
+  RSArgs a{};
+  a.dst = c->stage == 0 ? (void*)(c->grad + b.base + (uint64_t)c->rank * sl) : c->rs_dst(k);
+  a.count = sl;
+  a.n = c->n_d;
+  a.dtype = c->pdt;
+  a.r32 = 0;
+  a.reduce = 0;
+  a.st = c->st;
+  a.part = c->part_comm;
+  a.slot = c->slots + c->slot_base[k];
+  CK(launch_reduce_scatter(a, grid_for((sl + 2047) / 2048, 4, c->sms), c->comm_stream));
+  c->launches++;
+  if (pooled) CK(cudaEventRecord(c->ev_pool_free[ps], c->comm_stream));
+  return finish_bucket_local(c, k);
+}
+
+}  // extern "C"
+
+namespace {
+
+zero_status issue_adam(zero_ctx* c, ZeroGroup* g) {
+  AdamArgs a{};
+  a.p32 = c->p32;
+  a.m = c->m;
+  a.v = c->v;
+  const bool g_in_grad = c->stage == 0 || (c->stage == 1 && !c->r32);
+  a.G = g_in_grad ? (const void*)c->grad : (const void*)c->gred;
+  a.g_dtype = c->r32 ? DT_F32 : c->pdt;
+  a.p_dtype = c->pdt;
+  if (g && (c->stage == 1 || c->stage == 2)) {  // fused all-gather: store into every replica
+    a.n_p16 = g->n;
+    for (int j = 0; j < g->n; ++j) a.p16[j] = g->ranks[j]->p16;
+  } else {
+    a.n_p16 = 1;
+    a.p16[0] = c->p16;
+  }
+  a.segs = c->segs;
+  a.n_segs = (int)c->segs_host.size();
+  a.total = c->S_e;
+  const int grid = grid_for((c->S_e + 2047) / 2048, 2, c->sms);
+  a.per_cta = align_up((c->S_e + grid - 1) / grid, 8);
+  a.beta1 = c->cfg.beta1;
+  a.beta2 = c->cfg.beta2;
+  a.eps = c->cfg.eps;
+  a.omb1 = 1.0f - c->cfg.beta1;
+  a.omb2 = 1.0f - c->cfg.beta2;
+  a.wd = c->cfg.weight_decay > 0.0f ? 1 : 0;
+  a.lrwd = (float)((double)c->cfg.lr * (double)c->cfg.weight_decay);
+  a.st = c->st;
+  CK(launch_adam(a, grid, c->comm_stream));
+  c->launches++;
+  c->adam_launches++;
+  return ZERO_OK;
+}
+
+DecideParams decide_params(const zero_ctx* c) {
+  DecideParams p{};
+  p.n_ranks = c->n_d;
+  p.dynamic = c->cfg.dynamic_loss_scale ? 1 : 0;
+  p.beta1 = c->cfg.beta1;
+  p.beta2 = c->cfg.beta2;
+  p.lr = c->cfg.lr;
+  p.max_norm = c->cfg.max_grad_norm;
+  p.min_scale = c->cfg.min_loss_scale;
+  p.sigma = c->cfg.grad_prescale;
+  p.window = c->cfg.scale_window;
+  return p;
+}
+
+void reset_step(zero_ctx* c) {
+  std::fill(c->reduced.begin(), c->reduced.end(), 0);
+  c->n_reduced = 0;
+  std::fill(c->pool_pending.begin(), c->pool_pending.end(), -1);
+}
+
+}  // namespace
+
+extern "C" {
+
+zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
+  STICKY(c);
+  if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
+  ZeroGroup* g = c->group;
+  if (g) {
+    if (g->reduced_buckets != c->info.n_buckets)
+      return c->fail(ZERO_ESTATE, "zero_step before every bucket was reduced by every rank (%u of %u)",
+                     g->reduced_buckets, c->info.n_buckets);
+    if (c->stepped_this_round) return c->fail(ZERO_ESTATE, "rank already stepped this round");
+  } else if (c->n_reduced != c->info.n_buckets) {
+    return c->fail(ZERO_ESTATE, "zero_step before every bucket was reduced (%u of %u)", c->n_reduced,
+                   c->info.n_buckets);
+  }
+
+  zero_ctx::StepEvents* ev = nullptr;
+  if (c->cfg.timing && c->step_open) {
+    ev = &c->ev_pool[c->ev_used];
+    CK(cudaEventRecord(ev->r1, c->comm_stream));
+  }
+  PartialPtrs pp{};
+  if (c->transport == ZERO_TRANSPORT_LOCAL) {
+    CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream));
+    c->launches++;
+    pp.p[0] = c->my_partial;
+  } else if (c->transport == ZERO_TRANSPORT_PEER) {
+    for (int j = 0; j < g->n; ++j) pp.p[j] = g->ranks[j]->my_partial;
+  } else {
+    CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream));
+    c->launches++;
+    NK(ncclAllGather(c->my_partial, c->gathered, 2, ncclFloat64, c->comm, c->comm_stream));
+    for (int j = 0; j < c->n_d; ++j) pp.p[j] = c->gathered + j;
+  }
+  CK(launch_decide_global(pp, c->st, decide_params(c), c->comm_stream));
+  c->launches++;
+  if (ev) CK(cudaEventRecord(ev->a0, c->comm_stream));
+  zero_status s = issue_adam(c, g);
+  if (s != ZERO_OK) return s;
+  if (ev) CK(cudaEventRecord(ev->a1, c->comm_stream));
+
+  if (c->transport == ZERO_TRANSPORT_NCCL && (c->stage == 1 || c->stage == 2)) {
+    // all-gather the updated 16-bit parameters per bucket, in place
+    const ncclDataType_t dt = nccl_dt(c->pdt);
+    NK(ncclGroupStart());
+    for (uint32_t k = 0; k < c->info.n_buckets; ++k) {
+      const zero_bucket& b = c->buckets[k];
+      const uint64_t sl = c->slice(k);
+      NK(ncclAllGather(c->p16 + b.base + (uint64_t)c->rank * sl, c->p16 + b.base, sl, dt, c->comm, c->comm_stream));
+      c->counters.all_gather += sl * (uint64_t)(c->n_d - 1);
+    }
+    NK(ncclGroupEnd());
+  } else if (c->transport == ZERO_TRANSPORT_PEER && (c->stage == 1 || c->stage == 2)) {
+    for (uint32_t k = 0; k < c->info.n_buckets; ++k) c->counters.all_gather += c->slice(k) * (uint64_t)(c->n_d - 1);
+  }
+  if (host_out)
+    CK(cudaMemcpyAsync(host_out, &c->st->rec_t, sizeof(zero_step_info), cudaMemcpyDeviceToHost, c->comm_stream));
+  if (ev) {
+    CK(cudaEventRecord(ev->s1, c->comm_stream));
+    c->ev_used++;
+    c->step_open = false;
+  }
+  if (c->comm_stream != c->stream) {
+    CK(cudaEventRecord(c->ev_step, c->comm_stream));
+    CK(cudaStreamWaitEvent(c->stream, c->ev_step, 0));
+  }
+  c->counters.steps++;
+  if (g) {
+    c->stepped_this_round = true;
+    if (++g->stepped == g->n) {
+      for (int j = 0; j < g->n; ++j) {
+        reset_step(g->ranks[j]);
+        g->ranks[j]->stepped_this_round = false;
+      }
+      std::fill(g->flat_count.begin(), g->flat_count.end(), 0);
+      g->reduced_buckets = 0;
+      g->stepped = 0;
+    }
+  } else {
+    reset_step(c);
+  }
+  return ZERO_OK;
+}
+
+zero_status zero_sim_group(zero_ctx* const* ranks, int n) {
+  if (!ranks || n < 2 || n > ZERO_MAX_RANKS) return ZERO_EINVAL;
+  for (int r = 0; r < n; ++r) {
+    zero_ctx* c = ranks[r];
+    if (!c || c->rank != r || c->n_d != n || c->transport != ZERO_TRANSPORT_PEER || !c->bound || c->group)
+      return ZERO_EINVAL;
+    if (c->stage != ranks[0]->stage || c->stream != ranks[0]->stream || c->info.psi_padded != ranks[0]->info.psi_padded ||
+        c->info.n_buckets != ranks[0]->info.n_buckets || c->pdt != ranks[0]->pdt || c->r32 != ranks[0]->r32)
+      return c->fail(ZERO_EINVAL, "group members differ in stage/stream/layout/dtype");
+  }
+  ZeroGroup* g = new ZeroGroup();
+  g->n = n;
+  g->flat_count.assign(ranks[0]->info.n_buckets, 0);
+  for (int r = 0; r < n; ++r) {
+    g->ranks[r] = ranks[r];
+    ranks[r]->group = g;
+  }
+  return ZERO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// stage 3: per-layer gather with prefetch
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+namespace {
+
+zero_status issue_layer_gather(zero_ctx* c, int li, int slot) {
+  const LayerInfo& L = c->layers[li];
+  GatherSlot& gs = c->gslots[slot];
+  uint16_t* dst = c->gather + (uint64_t)slot * c->max_layer;
+  if (c->transport == ZERO_TRANSPORT_NCCL) {
+    CK(cudaStreamWaitEvent(c->comm_stream, gs.freed, 0));
+    NK(ncclGroupStart());
+    for (uint32_t k = L.k0; k < L.k1; ++k) {
+      const zero_bucket& b = c->buckets[k];
+      const uint64_t sl = c->slice(k);
+      NK(ncclAllGather(c->p16 + b.shard_off, dst + (b.base - L.flat0), sl, nccl_dt(c->pdt), c->comm, c->comm_stream));
+      c->counters.all_gather += sl * (uint64_t)(c->n_d - 1);
+    }
+    NK(ncclGroupEnd());
+    CK(cudaEventRecord(gs.ready, c->comm_stream));
+  } else {  // PEER: pull every rank's shard slice
+    ZeroGroup* g = c->group;
+    for (uint32_t k = L.k0; k < L.k1; ++k) {
+      const zero_bucket& b = c->buckets[k];
+      const uint64_t sl = c->slice(k);
+      CopyArgs a{};
+      for (int j = 0; j < g->n; ++j) {
+        a.src[j] = g->ranks[j]->p16 + b.shard_off;
+        a.dst[j] = dst + (b.base - L.flat0) + (uint64_t)j * sl;
+      }
+      a.count = sl;
+      a.n = g->n;
+      CK(launch_copy(a, grid_for((sl + 2047) / 2048, 2, c->sms), c->stream));
+      c->launches++;
+      c->counters.all_gather += sl * (uint64_t)(c->n_d - 1);
+    }
+  }
+  gs.layer = L.layer;
+  gs.released = false;
+  gs.lru = ++c->lru_clock;
+  c->layer_slot[li] = slot;
+  return ZERO_OK;
+}
+
+// a free slot: never used, or released; prefer the least recently used
+int free_slot(zero_ctx* c, int keep_li) {
+  int best = -1;
+  for (int s = 0; s < (int)c->gslots.size(); ++s) {
+    const GatherSlot& g = c->gslots[s];
+    if (!g.released) continue;
+    if (keep_li >= 0 && c->layer_slot[keep_li] == s) continue;
+    if (best < 0 || g.lru < c->gslots[best].lru) best = s;
+  }
+  if (best >= 0 && c->gslots[best].layer >= 0) {
+    auto it = c->layer_index.find((uint32_t)c->gslots[best].layer);
+    if (it != c->layer_index.end()) c->layer_slot[it->second] = -1;
+  }
+  return best;
+}
+
+}  // namespace
+
+extern "C" {
+
+zero_status zero_gather_params(zero_ctx* c, uint32_t layer, void** views_out) {
+  STICKY(c);
+  if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
+  if (c->stage != 3) return c->fail(ZERO_ESTATE, "zero_gather_params needs stage 3");
+  auto it = c->layer_index.find(layer);
+  if (it == c->layer_index.end()) return c->fail(ZERO_EINVAL, "unknown layer %u", layer);
+  const int li = it->second;
+  uint16_t* base;
+  if (c->n_d == 1) {
+    base = c->p16 + c->layers[li].flat0;  // the shard is the whole replica
+  } else {
+    if (c->last_layer >= 0) c->direction = (li >= c->last_layer) ? +1 : -1;
+    c->last_layer = li;
+    int s = c->layer_slot[li];
+    if (s < 0) {
+      s = free_slot(c, -1);
+      if (s < 0) return c->fail(ZERO_ESTATE, "gather pool exhausted: release layers before gathering more");
+      zero_status r = issue_layer_gather(c, li, s);
+      if (r != ZERO_OK) return r;
+    } else {
+      c->gslots[s].released = false;
+      c->gslots[s].lru = ++c->lru_clock;
+    }
+    // prefetch the next layers in the current direction into free slots
+    for (uint32_t d = 1; d <= c->cfg.prefetch_depth; ++d) {
+      const int nl = li + c->direction * (int)d;
+      if (nl < 0 || nl >= (int)c->layers.size() || c->layer_slot[nl] >= 0) continue;
+      const int fs = free_slot(c, li);
+      if (fs < 0) break;
+      zero_status r = issue_layer_gather(c, nl, fs);
+      if (r != ZERO_OK) return r;
+      c->gslots[fs].released = true;  // prefetched: reusable until someone asks for it
+    }
+    if (c->transport == ZERO_TRANSPORT_NCCL) CK(cudaStreamWaitEvent(c->stream, c->gslots[s].ready, 0));
+    base = c->gather + (uint64_t)s * c->max_layer;
+  }
+  if (views_out) {
+    const LayerInfo& L = c->layers[li];
+    for (uint32_t t = 0; t < c->tensors.size(); ++t)
+      if (c->tensors[t].layer == layer && c->tensors[t].numel > 0) views_out[t] = base + (c->tensor_flat[t] - L.flat0);
+  }
+  return ZERO_OK;
+}
+
+zero_status zero_release_params(zero_ctx* c, uint32_t layer) {
+  STICKY(c);
+  if (c->stage != 3) return c->fail(ZERO_ESTATE, "zero_release_params needs stage 3");
+  auto it = c->layer_index.find(layer);
+  if (it == c->layer_index.end()) return c->fail(ZERO_EINVAL, "unknown layer %u", layer);
+  if (c->n_d == 1) return ZERO_OK;
+  const int s = c->layer_slot[it->second];
+  if (s < 0) return c->fail(ZERO_ESTATE, "layer %u is not gathered", layer);
+  c->gslots[s].released = true;
+  if (c->transport == ZERO_TRANSPORT_NCCL) CK(cudaEventRecord(c->gslots[s].freed, c->stream));
+  return ZERO_OK;
+}
+
+zero_status zero_param_view(const zero_ctx* c, uint32_t t, void** p16) {
+  if (!c || !p16) return ZERO_EINVAL;
+  if (t >= c->tensors.size() || c->tensor_flat[t] == UINT64_MAX) return ZERO_EINVAL;
+  if (!c->bound) return ZERO_ESTATE;
+  if (c->stage == 3 && c->n_d > 1) return ZERO_ESTATE;
+  *p16 = c->p16 + c->tensor_flat[t];
+  return ZERO_OK;
+}
+
+zero_status zero_query(const zero_ctx* cc, int what, void* out, size_t n) {
+  zero_ctx* c = const_cast<zero_ctx*>(cc);
+  if (!c || !out) return ZERO_EINVAL;
+  switch (what) {
+    case ZERO_Q_LAYOUT:
+      if (n < sizeof(zero_layout_info)) return ZERO_EINVAL;
+      *reinterpret_cast<zero_layout_info*>(out) = c->info;
+      return ZERO_OK;
+    case ZERO_Q_BUCKETS:
+      if (n < sizeof(zero_bucket) * c->buckets.size()) return ZERO_EINVAL;
+      std::memcpy(out, c->buckets.data(), sizeof(zero_bucket) * c->buckets.size());
+      return ZERO_OK;
+    case ZERO_Q_PIECES:
+      if (n < sizeof(zero_piece) * c->pieces.size()) return ZERO_EINVAL;
+      std::memcpy(out, c->pieces.data(), sizeof(zero_piece) * c->pieces.size());
+      return ZERO_OK;
+    case ZERO_Q_MEMORY: {
+      if (n < sizeof(zero_memory)) return ZERO_EINVAL;
+      zero_memory mem{};
+      const zero_sizes& z = c->sizes;
+      const uint64_t S = c->info.shard;
+      mem.params16 = z.p16_bytes;
+      mem.optimizer = z.opt_bytes;
+      if (c->stage <= 1) {
+        mem.grads16 = z.grad_bytes;
+        mem.reduced_grad_extra = z.gred_bytes;
+      } else {
+        mem.grads16 = 2 * S;
+        mem.reduced_grad_extra = z.gred_bytes - 2 * S;
+        mem.staging = z.grad_bytes;
+      }
+      mem.gather_pool = z.gather_bytes;
+      mem.scratch = z.scratch_bytes;
+      *reinterpret_cast<zero_memory*>(out) = mem;
+      return ZERO_OK;
+    }
+    case ZERO_Q_COMM:
+      if (n < sizeof(zero_comm_counters)) return ZERO_EINVAL;
+      *reinterpret_cast<zero_comm_counters*>(out) = c->counters;
+      return ZERO_OK;
+    case ZERO_Q_STEP: {
+      if (n < sizeof(zero_step_info)) return ZERO_EINVAL;
+      if (!c->bound) return ZERO_ESTATE;
+      STICKY(c);
+      CK(cudaStreamSynchronize(c->comm_stream));
+      CK(cudaStreamSynchronize(c->stream));
+      CK(cudaMemcpy(out, &c->st->rec_t, sizeof(zero_step_info), cudaMemcpyDeviceToHost));
+      return ZERO_OK;
+    }
+    case ZERO_Q_STATE: {
+      if (n < sizeof(zero_device_state)) return ZERO_EINVAL;
+      if (!c->bound) return ZERO_ESTATE;
+      STICKY(c);
+      CK(cudaStreamSynchronize(c->comm_stream));
+      CK(cudaStreamSynchronize(c->stream));
+      DevState d{};
+      CK(cudaMemcpy(&d, c->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+      zero_device_state o{};
+      o.b1t = d.b1t;
+      o.b2t = d.b2t;
+      o.t = d.t;
+      o.loss_scale = d.S;
+      o.good_steps = d.good;
+      *reinterpret_cast<zero_device_state*>(out) = o;
+      return ZERO_OK;
+    }
+    case ZERO_Q_TIMING: {
+      if (n < sizeof(zero_timing)) return ZERO_EINVAL;
+      STICKY(c);
+      zero_timing tm{};
+      if (c->bound && c->ev_used) {
+        CK(cudaStreamSynchronize(c->comm_stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (size_t i = 0; i < c->ev_used; ++i) {
+          float a = 0, b = 0, d = 0;
+          CK(cudaEventElapsedTime(&a, c->ev_pool[i].r0, c->ev_pool[i].r1));
+          CK(cudaEventElapsedTime(&b, c->ev_pool[i].a0, c->ev_pool[i].a1));
+          CK(cudaEventElapsedTime(&d, c->ev_pool[i].r1, c->ev_pool[i].s1));
+          tm.reduce_ms += a;
+          tm.adam_ms += b;
+          tm.step_ms += d;
+        }
+        tm.steps = c->ev_used;
+        c->ev_used = 0;
+      }
+      tm.kernel_launches = c->launches;
+      tm.adam_launches = c->adam_launches;
+      *reinterpret_cast<zero_timing*>(out) = tm;
+      return ZERO_OK;
+    }
+    default:
+      return ZERO_EINVAL;
+  }
+}
+
+const char* zero_last_error(const zero_ctx* c) {
+  if (!c) return g_init_error.c_str();
+  return c->err.c_str();
+}
+
+void zero_destroy(zero_ctx* c) {
+  if (!c) return;
+  if (c->bound) {
+    cudaStreamSynchronize(c->stream);
+    if (c->comm_stream && c->comm_stream != c->stream) cudaStreamSynchronize(c->comm_stream);
+  }
+  if (c->group) {  // the group dissolves with its first destroyed member
+    ZeroGroup* g = c->group;
+    for (int j = 0; j < g->n; ++j)
+      if (g->ranks[j]) g->ranks[j]->group = nullptr;
+    delete g;
+  }
+  for (auto& e : c->ev_pool_free) if (e) cudaEventDestroy(e);
+  for (auto& e : c->ev_pool) {
+    cudaEventDestroy(e.r0);
+    cudaEventDestroy(e.r1);
+    cudaEventDestroy(e.a0);
+    cudaEventDestroy(e.a1);
+    cudaEventDestroy(e.s1);
+  }
+  for (auto& gs : c->gslots) {
+    if (gs.ready) cudaEventDestroy(gs.ready);
+    if (gs.freed) cudaEventDestroy(gs.freed);
+  }
+  if (c->ev_flat) cudaEventDestroy(c->ev_flat);
+  if (c->ev_step) cudaEventDestroy(c->ev_step);
+  if (c->ev_tmp) cudaEventDestroy(c->ev_tmp);
+  if (c->own_comm_stream && c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,654 @@
+// sm_100a kernels of the ZeRO-DP hot path (arXiv 1910.02054).
+//
+// Every kernel here is a bandwidth-bound streaming pass (no dense
+// contraction on the path, so no tensor cores).  Design rules applied:
+//  * 256-bit (LDG.E.256 / STG.E.256) accesses for fp32 streams and 128-bit for
+//    16-bit streams, with L1::no_allocate (no reuse within a step);
+//  * persistent grids sized from the SM count; contiguous per-CTA ranges;
+//  * reductions (overflow flag, sum of squares for the global grad norm)
+//    are warp-shuffle + shared-memory trees in fp64 with a last-CTA combine in a
+//    fixed order, so results are deterministic run to run;
+//  * fp32 arithmetic uses the __f*_rn intrinsics in the op order of reading c-3
+//    (never contracted to FMA), conversions are cvt.rn (reading c-5).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+#include "zero_internal.h"
+
+namespace zero {
+
+// ---------------------------------------------------------------------------
+// 16-bit formats
+// ---------------------------------------------------------------------------
+template <int DT>
+struct H16;
+template <>
+struct H16<DT_F16> {
+  static __device__ __forceinline__ float widen(uint32_t b) { return __half2float(__ushort_as_half((unsigned short)b)); }
+  static __device__ __forceinline__ uint32_t narrow(float x) { return __half_as_ushort(__float2half_rn(x)); }
+  static __device__ __forceinline__ uint32_t nonfinite(uint32_t b) { return (b & 0x7C00u) == 0x7C00u; }
+};
+template <>
+struct H16<DT_BF16> {
+  static __device__ __forceinline__ float widen(uint32_t b) { return __uint_as_float(b << 16); }
+  static __device__ __forceinline__ uint32_t narrow(float x) { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); }
+  static __device__ __forceinline__ uint32_t nonfinite(uint32_t b) { return (b & 0x7F80u) == 0x7F80u; }
+};
+
+// ---------------------------------------------------------------------------
+// streaming vector accesses
+// ---------------------------------------------------------------------------
+struct U8 { uint32_t x[8]; };
+struct U4 { uint32_t x[4]; };
+
+__device__ __forceinline__ U8 ld256(const void* p) {
+  U8 r;
+  asm volatile("ld.global.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.x[0]), "=r"(r.x[1]), "=r"(r.x[2]), "=r"(r.x[3]), "=r"(r.x[4]), "=r"(r.x[5]),
+                 "=r"(r.x[6]), "=r"(r.x[7])
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st256(void* p, const U8& r) {
+  asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r.x[0]),
+               "r"(r.x[1]), "r"(r.x[2]), "r"(r.x[3]), "r"(r.x[4]), "r"(r.x[5]), "r"(r.x[6]), "r"(r.x[7])
+               : "memory");
+}
+__device__ __forceinline__ U4 ld128(const void* p) {
+  U4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x[0]), "=r"(r.x[1]), "=r"(r.x[2]), "=r"(r.x[3])
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st128(void* p, const U4& r) {
+  asm volatile("st.global.L1::no_allocate.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(r.x[0]), "r"(r.x[1]),
+               "r"(r.x[2]), "r"(r.x[3])
+               : "memory");
+}
+__host__ __device__ __forceinline__ bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+// 8 16-bit values packed in a U4
+__device__ __forceinline__ uint32_t h_get(const U4& v, int j) { return (v.x[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu; }
+__device__ __forceinline__ void h_set(U4& v, int j, uint32_t b) {
+  if (j & 1) v.x[j >> 1] = (v.x[j >> 1] & 0x0000FFFFu) | (b << 16);
+  else v.x[j >> 1] = (v.x[j >> 1] & 0xFFFF0000u) | b;
+}
+
+// ---------------------------------------------------------------------------
+// deterministic fp64 sum + OR flag over a grid (last-CTA combine)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// returns the block total in thread 0 (fixed order: butterfly, then warps ascending)
+__device__ __forceinline__ void block_reduce(double& s, uint32_t& f) {
+  __shared__ double ws[32];
+  __shared__ uint32_t wf[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  s = warp_sum(s);
+  f = __reduce_or_sync(0xffffffffu, f);
+  __syncthreads();  // ws may be reused by a previous call
+  if (lane == 0) { ws[warp] = s; wf[warp] = f; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    uint32_t b = 0;
+    for (int i = 0; i < nw; ++i) { a += ws[i]; b |= wf[i]; }
+    s = a;
+    f = b;
+  }
+}
+
+__device__ void grid_publish(double s, uint32_t f, GridPartials* part, Slot* slot) {
+  __shared__ bool is_last;
+  block_reduce(s, f);
+  if (threadIdx.x == 0) {
+    part->sumsq[blockIdx.x] = s;
+    part->flag[blockIdx.x] = f;
+    __threadfence();
+    const unsigned t = atomicAdd(&part->ticket, 1u);
+    is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double a = 0.0;
+  uint32_t b = 0;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+    a += __ldcg(&part->sumsq[i]);
+    b |= __ldcg(&part->flag[i]);
+  }
+  block_reduce(a, b);
+  if (threadIdx.x == 0) {
+    slot->sumsq = a;
+    slot->flag = b;
+    part->ticket = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: flatten / cast / prescale one gradient bucket (a1), + epilogue at N_d = 1
+// ---------------------------------------------------------------------------
+constexpr int kFlatChunk = 4096;  // elements per chunk = 256 threads x 2 x 8
+
+template <int SDT>
+struct SrcLoad;
+template <>
+struct SrcLoad<DT_F16> {
+  static constexpr int kBytes = 2;
+  static __device__ __forceinline__ void vec(const void* p, float (&x)[8]) {
+    U4 v = ld128(p);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = H16<DT_F16>::widen(h_get(v, j));
+  }
+  static __device__ __forceinline__ float one(const void* p, uint64_t i) {
+    return H16<DT_F16>::widen(reinterpret_cast<const uint16_t*>(p)[i]);
+  }
+};
+template <>
+struct SrcLoad<DT_BF16> {
+  static constexpr int kBytes = 2;
+  static __device__ __forceinline__ void vec(const void* p, float (&x)[8]) {
+    U4 v = ld128(p);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = H16<DT_BF16>::widen(h_get(v, j));
+  }
+  static __device__ __forceinline__ float one(const void* p, uint64_t i) {
+    return H16<DT_BF16>::widen(reinterpret_cast<const uint16_t*>(p)[i]);
+  }
+};
+template <>
+struct SrcLoad<DT_F32> {
+  static constexpr int kBytes = 4;
+  static __device__ __forceinline__ void vec(const void* p, float (&x)[8]) {
+    U8 v = ld256(p);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = __uint_as_float(v.x[j]);
+  }
+  static __device__ __forceinline__ float one(const void* p, uint64_t i) { return reinterpret_cast<const float*>(p)[i]; }
+};
+
+// g' = RTNE16(widen(g) * sigma): a plain bit copy when sigma == 1 and the dtypes match
+template <int SDT, int DDT, bool kCopy>
+__global__ void __launch_bounds__(kThreads) k_flatten(const __grid_constant__ FlatArgs a) {
+  using S = SrcLoad<SDT>;
+  using D = H16<DDT>;
+  const float sigma = a.sigma;
+  const float inv = a.epilogue ? a.st->inv_cur : 0.0f;
+  double sumsq = 0.0;
+  uint32_t flag = 0;
+  uint16_t* dst_base = reinterpret_cast<uint16_t*>(a.dst);
+  for (uint64_t c = blockIdx.x; c < a.total_chunks; c += gridDim.x) {
+    int p = 0;
+    while (p + 1 < a.n_pieces && a.pieces[p + 1].chunk_begin <= c) ++p;
+    const FlatPiece pc = a.pieces[p];
+    const uint64_t e0 = (c - pc.chunk_begin) * (uint64_t)kFlatChunk;
+    const uint64_t rem = pc.count - e0;
+    const uint32_t n = rem < (uint64_t)kFlatChunk ? (uint32_t)rem : (uint32_t)kFlatChunk;
+    uint16_t* dst = dst_base + pc.dst_off + e0;
+    if (pc.src == nullptr) {  // alignment gap or bucket padding: zeros (reading c-7)
+      if (aligned(dst, 16)) {
+        for (uint32_t i = threadIdx.x * 8; i < n; i += kThreads * 8) {
+          if (i + 8 <= n) st128(dst + i, U4{{0u, 0u, 0u, 0u}});
+          else for (uint32_t j = i; j < n; ++j) dst[j] = 0;
+        }
+      } else {
+        for (uint32_t i = threadIdx.x; i < n; i += kThreads) dst[i] = 0;
+      }
+      continue;
+    }
+    const char* src = reinterpret_cast<const char*>(pc.src) + e0 * S::kBytes;
+    const bool vec = aligned(src, 8 * S::kBytes) && aligned(dst, 16);
+    auto emit_one = [&](uint32_t j) {
+      const float xv = S::one(src, j);
+      const uint32_t b = kCopy ? D::narrow(xv) : D::narrow(__fmul_rn(xv, sigma));
+      dst[j] = (uint16_t)b;
+      if (a.epilogue) {
+        flag |= D::nonfinite(b);
+        const float u = __fmul_rn(D::widen(b), inv);
+        sumsq += (double)u * (double)u;
+      }
+    };
+    auto emit8 = [&](uint32_t i, const float* x) {
+      U4 o;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t b = kCopy ? D::narrow(x[j]) : D::narrow(__fmul_rn(x[j], sigma));
+        h_set(o, j, b);
+        if (a.epilogue) {
+          flag |= D::nonfinite(b);
+          const float u = __fmul_rn(D::widen(b), inv);
+          sumsq += (double)u * (double)u;
+        }
+      }
+      st128(dst + i, o);
+    };
+    if (vec) {
+#pragma unroll 1
+      for (uint32_t i0 = threadIdx.x * 8; i0 < n; i0 += kThreads * 16) {
+        const uint32_t i1 = i0 + kThreads * 8;
+        float x0[8], x1[8];
+        const bool f0 = i0 + 8 <= n, f1 = i1 + 8 <= n;
+        if (f0) S::vec(src + (uint64_t)i0 * S::kBytes, x0);
+        if (f1) S::vec(src + (uint64_t)i1 * S::kBytes, x1);
+        if (f0) emit8(i0, x0);
+        else for (uint32_t j = i0; j < n; ++j) emit_one(j);
+        if (f1) emit8(i1, x1);
+        else for (uint32_t j = i1; j < n; ++j) emit_one(j);
+      }
+    } else {
+      for (uint32_t j = threadIdx.x; j < n; j += kThreads) emit_one(j);
+    }
+  }
+  if (a.epilogue) grid_publish(sumsq, flag, a.part, a.slot);
+}
+
+cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s) {
+  const bool copy = (a.sigma == 1.0f) && (a.src_dtype == a.dst_dtype);
+#define ZL(SD, DD, CP) k_flatten<SD, DD, CP><<<grid, kThreads, 0, s>>>(a)
+  if (a.dst_dtype == DT_F16) {
+    if (a.src_dtype == DT_F16) { if (copy) ZL(DT_F16, DT_F16, true); else ZL(DT_F16, DT_F16, false); }
+    else if (a.src_dtype == DT_F32) ZL(DT_F32, DT_F16, false);
+    else return cudaErrorInvalidValue;
+  } else if (a.dst_dtype == DT_BF16) {
+    if (a.src_dtype == DT_BF16) { if (copy) ZL(DT_BF16, DT_BF16, true); else ZL(DT_BF16, DT_BF16, false); }
+    else if (a.src_dtype == DT_F32) ZL(DT_F32, DT_BF16, false);
+    else return cudaErrorInvalidValue;
+  } else {
+    return cudaErrorInvalidValue;
+  }
+#undef ZL
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// a2+a3: pull reduce-scatter of one bucket slice over a peer table (fp32 sum in
+// ascending rank, one rounding for R16), fused with the overflow flag and the
+// norm partial.  reduce == 0: epilogue only (slice already reduced by NCCL).
+// ---------------------------------------------------------------------------
+template <int DT, bool kR32, bool kReduce, bool kVec>
+__global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_constant__ RSArgs a) {
+  using D = H16<DT>;
+  const float inv = a.st->inv_cur;
+  double sumsq = 0.0;
+  uint32_t flag = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads * (kVec ? 8 : 1);
+  for (uint64_t i = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) * (kVec ? 8 : 1); i < a.count; i += stride) {
+    if (kVec && i + 8 <= a.count) {
+      float acc[8];
+      if (kReduce) {
+        U4 v[kMaxRanks];
+#pragma unroll
+        for (int r = 0; r < kMaxRanks; ++r)
+          if (r < a.n) v[r] = ld128(reinterpret_cast<const uint16_t*>(a.src[r]) + i);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = D::widen(h_get(v[0], j));
+#pragma unroll
+        for (int r = 1; r < kMaxRanks; ++r)
+          if (r < a.n) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], D::widen(h_get(v[r], j)));
+          }
+      } else if (kR32) {
+        U8 w = ld256(reinterpret_cast<const float*>(a.dst) + i);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = __uint_as_float(w.x[j]);
+      } else {
+        U4 w = ld128(reinterpret_cast<const uint16_t*>(a.dst) + i);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = D::widen(h_get(w, j));
+      }
+      if (kR32) {
+        U8 o;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          o.x[j] = __float_as_uint(acc[j]);
+          flag |= (uint32_t)!isfinite(acc[j]);
+          const float u = __fmul_rn(acc[j], inv);
+          sumsq += (double)u * (double)u;
+        }
+        if (kReduce) st256(reinterpret_cast<float*>(a.dst) + i, o);
+      } else {
+        U4 o;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t b = kReduce ? D::narrow(acc[j]) : D::narrow(acc[j]);
+          h_set(o, j, b);
+          flag |= D::nonfinite(b);
+          const float u = __fmul_rn(D::widen(b), inv);
+          sumsq += (double)u * (double)u;
+        }
+        if (kReduce) st128(reinterpret_cast<uint16_t*>(a.dst) + i, o);
+      }
+    } else {
+      const uint64_t e = kVec ? (a.count < i + 8 ? a.count : i + 8) : i + 1;
+      for (uint64_t k = i; k < e; ++k) {
+        float acc;
+        if (kReduce) {
+          acc = D::widen(reinterpret_cast<const uint16_t*>(a.src[0])[k]);
+          for (int r = 1; r < a.n; ++r) acc = __fadd_rn(acc, D::widen(reinterpret_cast<const uint16_t*>(a.src[r])[k]));
+        } else if (kR32) {
+          acc = reinterpret_cast<const float*>(a.dst)[k];
+        } else {
+          acc = D::widen(reinterpret_cast<const uint16_t*>(a.dst)[k]);
+        }
+        float G;
+        if (kR32) {
+          G = acc;
+          flag |= (uint32_t)!isfinite(acc);
+          if (kReduce) reinterpret_cast<float*>(a.dst)[k] = acc;
+        } else {
+          const uint32_t b = D::narrow(acc);
+          G = D::widen(b);
+          flag |= D::nonfinite(b);
+          if (kReduce) reinterpret_cast<uint16_t*>(a.dst)[k] = (uint16_t)b;
+        }
+        const float u = __fmul_rn(G, inv);
+        sumsq += (double)u * (double)u;
+      }
+    }
+  }
+  grid_publish(sumsq, flag, a.part, a.slot);
+}
+
+cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s) {
+  bool vec = aligned(a.dst, a.r32 ? 32 : 16);
+  if (a.reduce)
+    for (int r = 0; r < a.n; ++r) vec = vec && aligned(a.src[r], 16);
+#define ZR(DT, R32, RED, V) k_reduce_scatter<DT, R32, RED, V><<<grid, kThreads, 0, s>>>(a)
+#define ZRV(DT, R32, RED) do { if (vec) ZR(DT, R32, RED, true); else ZR(DT, R32, RED, false); } while (0)
+#define ZRR(DT, R32) do { if (a.reduce) ZRV(DT, R32, true); else ZRV(DT, R32, false); } while (0)
+  if (a.dtype == DT_F16) { if (a.r32) ZRR(DT_F16, true); else ZRR(DT_F16, false); }
+  else if (a.dtype == DT_BF16) { if (a.r32) ZRR(DT_BF16, true); else ZRR(DT_BF16, false); }
+  else return cudaErrorInvalidValue;
+#undef ZRR
+#undef ZRV
+#undef ZR
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// a4: global decision (reading c-4).  decide_local folds this rank's per-bucket
+// slots (ascending bucket, fixed tree) into one RankPartial; decide_global folds
+// the ranks' partials in ascending rank and advances the loss-scale machine.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_decide_local(const Slot* slots, int n, RankPartial* out) {
+  double s = 0.0;
+  uint32_t f = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    s += slots[i].sumsq;
+    f |= slots[i].flag;
+  }
+  block_reduce(s, f);
+  if (threadIdx.x == 0) {
+    out->sumsq = s;
+    out->flag = f ? 1.0 : 0.0;
+  }
+}
+
+cudaError_t launch_decide_local(const Slot* slots, int n_slots, RankPartial* out, cudaStream_t s) {
+  k_decide_local<<<1, kThreads, 0, s>>>(slots, n_slots, out);
+  return cudaGetLastError();
+}
+
+__global__ void k_decide_global(const __grid_constant__ PartialPtrs pp, DevState* st, const DecideParams p) {
+  if (threadIdx.x != 0) return;
+  double sum = 0.0, flags = 0.0;
+  for (int r = 0; r < p.n_ranks; ++r) {
+    sum += pp.p[r]->sumsq;
+    flags += pp.p[r]->flag;
+  }
+  const bool overflow = flags != 0.0;
+  const float S_used = st->S;
+  const double norm = sqrt(sum);
+  float clip = 1.0f;
+  if (overflow) {
+    st->skip = 1u;
+    if (p.dynamic) {
+      st->S = fmaxf(st->S * 0.5f, p.min_scale);
+      st->good = 0;
+    }
+  } else {
+    if (p.max_norm > 0.0f && norm > (double)p.max_norm) clip = (float)((double)p.max_norm / (norm + 1e-6));
+    st->t += 1;
+    st->b1t *= (double)p.beta1;
+    st->b2t *= (double)p.beta2;
+    st->step_f = (float)((double)p.lr / (1.0 - st->b1t));
+    st->rsb2_f = (float)(1.0 / sqrt(1.0 - st->b2t));
+    st->clip_f = clip;
+    st->inv_adam = st->inv_cur;
+    st->skip = 0u;
+    if (p.dynamic) {
+      st->good += 1;
+      if (st->good == p.window) {
+        st->S = st->S * 2.0f;
+        st->good = 0;
+      }
+    }
+  }
+  st->inv_cur = (float)(1.0 / ((double)p.n_ranks * (double)st->S * (double)p.sigma));
+  st->rec_t = st->t;
+  st->rec_overflow = overflow ? 1u : 0u;
+  st->rec_scale = S_used;
+  st->rec_clip = clip;
+  st->rec_pad = 0;
+  st->rec_norm = norm;
+}
+
+cudaError_t launch_decide_global(const PartialPtrs& partials, DevState* st, DecideParams p, cudaStream_t s) {
+  k_decide_global<<<1, 32, 0, s>>>(partials, st, p);
+  return cudaGetLastError();
+}
+
+__global__ void k_init_state(DevState* st, float S, float inv) {
+  st->b1t = 1.0;
+  st->b2t = 1.0;
+  st->t = 0;
+  st->S = S;
+  st->good = 0;
+  st->inv_cur = inv;
+  st->inv_adam = inv;
+  st->step_f = 0.0f;
+  st->rsb2_f = 1.0f;
+  st->clip_f = 1.0f;
+  st->skip = 1u;
+  st->rec_t = 0;
+  st->rec_overflow = 0;
+  st->rec_scale = S;
+  st->rec_clip = 1.0f;
+  st->rec_pad = 0;
+  st->rec_norm = 0.0;
+}
+
+cudaError_t launch_init_state(DevState* st, float S, float inv, cudaStream_t s) {
+  k_init_state<<<1, 1, 0, s>>>(st, S, inv);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// a5: fused partitioned Adam + 16-bit recast, stored straight into the
+// all-gather buffer(s) ("only update 1/N_d of the parameters").
+// 28 B/element (R16): read p32, m, v (12 B) + G (2 B); write p32, m, v + p16.
+// ---------------------------------------------------------------------------
+struct AdamScalars {
+  float inv, step, rsb2, clip, beta1, beta2, eps, omb1, omb2, lrwd;
+  int wd;
+};
+
+__device__ __forceinline__ void adam_elem(float& p, float& m, float& v, float G, const AdamScalars& c) {
+  float g = __fmul_rn(G, c.inv);
+  if (c.clip != 1.0f) g = __fmul_rn(g, c.clip);
+  if (c.wd) p = __fsub_rn(p, __fmul_rn(c.lrwd, p));
+  m = __fadd_rn(__fmul_rn(c.beta1, m), __fmul_rn(c.omb1, g));
+  v = __fadd_rn(__fmul_rn(c.beta2, v), __fmul_rn(__fmul_rn(c.omb2, g), g));
+  const float d = __fadd_rn(__fmul_rn(__fsqrt_rn(v), c.rsb2), c.eps);
+  p = __fsub_rn(p, __fmul_rn(c.step, __fdiv_rn(m, d)));
+}
+
+template <int PDT, int GDT>
+__global__ void __launch_bounds__(kThreads, 2) k_adam(const __grid_constant__ AdamArgs a) {
+  using P = H16<PDT>;
+  if (a.st->skip) return;  // overflow: the whole step is skipped (reading c-4)
+  AdamScalars c;
+  c.inv = a.st->inv_adam;
+  c.step = a.st->step_f;
+  c.rsb2 = a.st->rsb2_f;
+  c.clip = a.st->clip_f;
+  c.beta1 = a.beta1;
+  c.beta2 = a.beta2;
+  c.eps = a.eps;
+  c.omb1 = a.omb1;
+  c.omb2 = a.omb2;
+  c.lrwd = a.lrwd;
+  c.wd = a.wd;
+  const uint64_t lo = (uint64_t)blockIdx.x * a.per_cta;
+  if (lo >= a.total) return;
+  const uint64_t hi = lo + a.per_cta < a.total ? lo + a.per_cta : a.total;
+  // first segment containing lo (segments sorted by local_off, tiling [0, total))
+  int s0 = 0, s1 = a.n_segs - 1;
+  while (s0 < s1) {
+    const int mid = (s0 + s1 + 1) >> 1;
+    if (a.segs[mid].local_off <= lo) s0 = mid; else s1 = mid - 1;
+  }
+  uint64_t cur = lo;
+  for (int s = s0; cur < hi && s < a.n_segs; ++s) {
+    const AdamSeg sg = a.segs[s];
+    const uint64_t send = sg.local_off + sg.count < hi ? sg.local_off + sg.count : hi;
+    if (send <= cur) continue;
+    const int64_t gd = (int64_t)sg.g_off - (int64_t)sg.local_off;
+    const int64_t pd = (int64_t)sg.p16_off - (int64_t)sg.local_off;
+    uint64_t vend = cur;
+    if (((cur | (uint64_t)gd | (uint64_t)pd) & 7) == 0) {
+      vend = cur + ((send - cur) & ~(uint64_t)7);
+#pragma unroll 1
+      for (uint64_t i = cur + threadIdx.x * 8; i < vend; i += kThreads * 8) {
+        U8 p = ld256(a.p32 + i);
+        U8 m = ld256(a.m + i);
+        U8 v = ld256(a.v + i);
+        float G[8];
+        if (GDT == DT_F32) {
+          U8 g = ld256(reinterpret_cast<const float*>(a.G) + (i + gd));
+#pragma unroll
+          for (int j = 0; j < 8; ++j) G[j] = __uint_as_float(g.x[j]);
+        } else {
+          U4 g = ld128(reinterpret_cast<const uint16_t*>(a.G) + (i + gd));
+#pragma unroll
+          for (int j = 0; j < 8; ++j) G[j] = H16<GDT == DT_F32 ? DT_F16 : GDT>::widen(h_get(g, j));
+        }
+        U4 o;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float pj = __uint_as_float(p.x[j]), mj = __uint_as_float(m.x[j]), vj = __uint_as_float(v.x[j]);
+          adam_elem(pj, mj, vj, G[j], c);
+          p.x[j] = __float_as_uint(pj);
+          m.x[j] = __float_as_uint(mj);
+          v.x[j] = __float_as_uint(vj);
+          h_set(o, j, P::narrow(pj));
+        }
+        st256(a.p32 + i, p);
+        st256(a.m + i, m);
+        st256(a.v + i, v);
+        for (int d = 0; d < a.n_p16; ++d) st128(reinterpret_cast<uint16_t*>(a.p16[d]) + (i + pd), o);
+      }
+    }
+    for (uint64_t i = vend + threadIdx.x; i < send; i += kThreads) {  // unaligned remainder
+      float p = a.p32[i], m = a.m[i], v = a.v[i];
+      float G;
+      if (GDT == DT_F32) G = reinterpret_cast<const float*>(a.G)[i + gd];
+      else G = H16<GDT == DT_F32 ? DT_F16 : GDT>::widen(reinterpret_cast<const uint16_t*>(a.G)[i + gd]);
+      adam_elem(p, m, v, G, c);
+      a.p32[i] = p;
+      a.m[i] = m;
+      a.v[i] = v;
+      const uint16_t b = (uint16_t)P::narrow(p);
+      for (int d = 0; d < a.n_p16; ++d) reinterpret_cast<uint16_t*>(a.p16[d])[i + pd] = b;
+    }
+    cur = send;
+  }
+}
+
+cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s) {
+#define ZA(PD, GD) k_adam<PD, GD><<<grid, kThreads, 0, s>>>(a)
+  if (a.p_dtype == DT_F16) {
+    if (a.g_dtype == DT_F16) ZA(DT_F16, DT_F16);
+    else if (a.g_dtype == DT_F32) ZA(DT_F16, DT_F32);
+    else return cudaErrorInvalidValue;
+  } else if (a.p_dtype == DT_BF16) {
+    if (a.g_dtype == DT_BF16) ZA(DT_BF16, DT_BF16);
+    else if (a.g_dtype == DT_F32) ZA(DT_BF16, DT_F32);
+    else return cudaErrorInvalidValue;
+  } else {
+    return cudaErrorInvalidValue;
+  }
+#undef ZA
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// a6/a7 over a peer table: dst[j][0..count) = src[j][0..count) (16-bit, bitwise)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ CopyArgs a) {
+  const int j = blockIdx.y;
+  const uint16_t* src = reinterpret_cast<const uint16_t*>(a.src[j]);
+  uint16_t* dst = reinterpret_cast<uint16_t*>(a.dst[j]);
+  if (src == dst) return;
+  const uint64_t tid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  const uint64_t nthr = (uint64_t)gridDim.x * kThreads;
+  if (aligned(src, 16) && aligned(dst, 16)) {
+    const uint64_t nv = a.count / 8;
+    for (uint64_t i = tid; i < nv; i += nthr) st128(dst + i * 8, ld128(src + i * 8));
+    for (uint64_t i = nv * 8 + tid; i < a.count; i += nthr) dst[i] = src[i];
+  } else {
+    for (uint64_t i = tid; i < a.count; i += nthr) dst[i] = src[i];
+  }
+}
+
+cudaError_t launch_copy(const CopyArgs& a, int grid, cudaStream_t s) {
+  if (a.n <= 0 || a.count == 0) return cudaSuccess;
+  dim3 g(grid, a.n);
+  k_copy<<<g, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// zero_load_master: fp32 master piece -> owned fp32 shard + 16-bit copy
+// ---------------------------------------------------------------------------
+template <int PDT>
+__global__ void __launch_bounds__(kThreads) k_load(const __grid_constant__ LoadArgs a) {
+  using P = H16<PDT>;
+  uint16_t* p16 = reinterpret_cast<uint16_t*>(a.p16);
+  for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < a.count; i += (uint64_t)gridDim.x * kThreads) {
+    const float x = a.src[i];
+    const uint64_t g = a.flat_off + i;
+    const uint16_t b = (uint16_t)P::narrow(x);
+    if (a.p16_mode == 0) p16[g] = b;
+    if (g >= a.own_lo && g < a.own_hi) {
+      const uint64_t l = a.local_base + (g - a.own_lo);
+      a.p32[l] = x;
+      if (a.p16_mode == 1) p16[l] = b;
+    }
+  }
+}
+
+cudaError_t launch_load(const LoadArgs& a, cudaStream_t s) {
+  if (a.count == 0) return cudaSuccess;
+  uint64_t blocks = (a.count + kThreads - 1) / kThreads;
+  const int grid = (int)(blocks < 4096 ? blocks : 4096);
+  if (a.p_dtype == DT_F16) k_load<DT_F16><<<grid, kThreads, 0, s>>>(a);
+  else k_load<DT_BF16><<<grid, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+}  // namespace zero

@@ -1,0 +1,149 @@
+// Internal types shared by the host engine (engine.cpp) and the sm_100a kernels
+// (kernels.cu).  Not part of the ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace zero {
+
+constexpr int kMaxRanks = 8;
+constexpr int kMaxFlatPieces = 32;      // pieces per flatten launch (kernel-parameter table)
+constexpr int kMaxGrid = 1184;          // 148 SMs x 8: upper bound of any reduction grid
+constexpr int kThreads = 256;
+
+enum DType : int { DT_F16 = 0, DT_BF16 = 1, DT_F32 = 2 };
+
+// Per-bucket epilogue result: overflow flag and sum of (G*inv)^2 (fp64).
+struct Slot {
+  double sumsq;
+  uint32_t flag;
+  uint32_t pad;
+};
+
+// Per-rank partial combined across ranks by the decision kernel.
+struct RankPartial {
+  double sumsq;
+  double flag;   // 0 or 1 (double so the record is one 16-byte all-gather)
+};
+
+// Scratch for the deterministic last-CTA reduction of a grid.
+struct GridPartials {
+  double sumsq[kMaxGrid];
+  uint32_t flag[kMaxGrid];
+  uint32_t ticket;
+  uint32_t pad;
+};
+
+// Loss-scale / Adam scalars living on the device (reading c-4).  Only the decision
+// kernel writes them; epilogues and Adam read them.
+struct DevState {
+  double b1t, b2t;          // running beta^t products (fp64)
+  uint64_t t;               // Adam step count
+  float S;                  // current loss scale
+  uint32_t good;            // consecutive good steps
+  float inv_cur;            // inv = fp32(1/(N*S*sigma)) for the current step's epilogues
+  float inv_adam;           // inv of the step being applied (latched by the decision)
+  float step_f, rsb2_f, clip_f;
+  uint32_t skip;            // 1: overflow -> Adam exits
+  // step record (mirrors zero_step_info, 32 bytes)
+  uint64_t rec_t;
+  uint32_t rec_overflow;
+  float rec_scale;
+  float rec_clip;
+  uint32_t rec_pad;
+  double rec_norm;
+};
+
+struct DecideParams {
+  int n_ranks;
+  int dynamic;
+  float beta1, beta2, lr, max_norm, min_scale, sigma;
+  uint32_t window;
+};
+
+struct FlatPiece {
+  const void* src;          // nullptr = zero fill (alignment gap / padding)
+  uint64_t dst_off;         // element offset inside the destination bucket
+  uint64_t count;
+  uint64_t chunk_begin;     // prefix sum of chunks
+};
+
+struct FlatArgs {
+  FlatPiece pieces[kMaxFlatPieces];
+  int n_pieces;
+  int src_dtype, dst_dtype;
+  int epilogue;             // 1: also compute the overflow flag and norm partial (N_d == 1)
+  uint64_t total_chunks;
+  void* dst;
+  float sigma;
+  const DevState* st;
+  GridPartials* part;
+  Slot* slot;
+};
+
+struct RSArgs {
+  const void* src[kMaxRanks];   // rank j's bucket slice (16-bit)
+  void* dst;                    // reduced slice: 16-bit (R16) or fp32 (R32)
+  uint64_t count;
+  int n;
+  int dtype;                    // 16-bit dtype of the sources
+  int r32;                      // 1: write fp32
+  int reduce;                   // 0: epilogue only over dst (NCCL path: dst already reduced)
+  const DevState* st;
+  GridPartials* part;
+  Slot* slot;
+};
+
+struct AdamSeg {
+  uint64_t local_off, g_off, p16_off, count;
+};
+
+struct AdamArgs {
+  float* p32;
+  float* m;
+  float* v;
+  const void* G;
+  void* p16[kMaxRanks];     // destinations of the recast parameters (fused all-gather)
+  int n_p16;
+  int p_dtype, g_dtype;
+  const AdamSeg* segs;
+  int n_segs;
+  uint64_t total;           // elements in the shard
+  uint64_t per_cta;         // contiguous elements per CTA (multiple of 8)
+  float beta1, beta2, eps, omb1, omb2, lrwd;
+  int wd;
+  const DevState* st;
+};
+
+struct CopyArgs {             // multi-source 16-bit copy (pull all-gather)
+  const void* src[kMaxRanks];
+  void* dst[kMaxRanks];
+  uint64_t count;             // elements per source
+  int n;
+};
+
+struct LoadArgs {             // master init: fp32 piece -> shard / 16-bit copy
+  const float* src;
+  uint64_t count;
+  uint64_t flat_off;          // global flat offset of the piece's first element
+  uint64_t own_lo, own_hi;    // owned global range of the bucket (stage 0: whole bucket)
+  uint64_t local_base;        // shard offset of own_lo
+  float* p32;
+  void* p16;
+  int p16_mode;               // 0: replica at global index, 1: shard at local index
+  int p_dtype;
+};
+
+// launchers (kernels.cu); return the launch error
+cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_decide_local(const Slot* slots, int n_slots, RankPartial* out, cudaStream_t s);
+struct PartialPtrs { const RankPartial* p[kMaxRanks]; };
+cudaError_t launch_decide_global(const PartialPtrs& partials, DevState* st, DecideParams p, cudaStream_t s);
+cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_copy(const CopyArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_load(const LoadArgs& a, cudaStream_t s);
+cudaError_t launch_init_state(DevState* st, float S, float inv, cudaStream_t s);
+int sm_count();
+
+}  // namespace zero

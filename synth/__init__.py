@@ -173,6 +173,7 @@ def gpt_slice(tensors: Sequence[TensorSpec], n_layers: int) -> List[TensorSpec]:
 CONFIGS = {
     "mlp1m": mlp_layout,
     "gpt2_1.5b": gpt2_1p5b,
+    "gpt2_1.5b_l8": lambda: gpt_slice(gpt2_1p5b(), 8),   # first 8 layer groups (ncu captures)
     "gpt_7.5b": gpt_7p5b,
     "gpt_60b": gpt_60b,
 }
@@ -201,3 +202,70 @@ def masters32(tensors: Sequence[TensorSpec], seed: int):
     """fp32 master init as torch CPU tensors."""
     import torch
     return [torch.from_numpy(a) for a in master_values(tensors, seed)]
+
+
+# ---------------------------------------------------------------------------
+# device-side generation (same stream, re-implemented in synth/synth_fill.cu)
+# ---------------------------------------------------------------------------
+_SYNTH_LIB = None
+
+
+def _synth_lib():
+    global _SYNTH_LIB
+    if _SYNTH_LIB is None:
+        import ctypes as C
+        import os
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libzero_synth.so")
+        if not os.path.exists(path):
+            raise ImportError(f"{path} missing: run python -m paper_1910_02054_b200._build")
+        lib = C.CDLL(path)
+        lib.synth_fill.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_float, C.c_int,
+                                   C.c_int, C.c_float, C.c_void_p]
+        lib.synth_fill.restype = C.c_int
+        _SYNTH_LIB = lib
+    return _SYNTH_LIB
+
+
+def gpu_fill(out, key: int, start: int, scale: float, use_const: bool = False, const: float = 0.0, stream=None):
+    """out (a contiguous CUDA tensor, fp16/bf16/fp32) <- cast(x_{start+i} * scale)."""
+    import torch
+    code = {torch.float16: 0, torch.bfloat16: 1, torch.float32: 2}[out.dtype]
+    s = stream.cuda_stream if stream is not None else torch.cuda.current_stream(out.device).cuda_stream
+    rc = _synth_lib().synth_fill(out.data_ptr(), key, start, out.numel(), scale, code, 1 if use_const else 0,
+                                 const, s)
+    if rc != 0:
+        raise RuntimeError(f"synth_fill failed: cuda error {rc}")
+
+
+def gpu_masters(tensors: Sequence[TensorSpec], seed: int, device):
+    """fp32 master init on the device (same values as master_values)."""
+    import torch
+    key = stream_key(seed, KIND_MASTER)
+    out = []
+    for t, o in zip(tensors, tensor_offsets(tensors)):
+        a = torch.empty(t.numel, dtype=torch.float32, device=device)
+        if t.role == ROLE_LNW:
+            gpu_fill(a, key, o, 1.0, True, 1.0)
+        elif t.role == ROLE_BIAS:
+            gpu_fill(a, key, o, 1.0, True, 0.0)
+        else:
+            gpu_fill(a, key, o, 2.0 ** -6)
+        out.append(a)
+    return out
+
+
+def gpu_grads_flat(tensors: Sequence[TensorSpec], seed: int, rank: int, step: int, dtype, device,
+                   scale: float = 1.0, out=None):
+    """16-bit gradients of every tensor, as views of ONE contiguous device buffer
+    (unpadded concatenation, forward order) -- same values as grads16()."""
+    import torch
+    key = stream_key(seed, KIND_GRAD, rank, step)
+    offs = tensor_offsets(tensors)
+    total = psi(tensors)
+    buf = out if out is not None else torch.empty(total, dtype=dtype, device=device)
+    views = []
+    for ti, (t, o) in enumerate(zip(tensors, offs)):
+        v = buf[o:o + t.numel]
+        gpu_fill(v, key, o, (2.0 ** -(6 + (ti % 8))) * scale)
+        views.append(v)
+    return buf, views

@@ -1,0 +1,155 @@
+"""CPU tests of the C-ABI library (no GPU): it loads, exports every symbol the
+header declares, and its pure-host outputs (layout, memory arenas, volume closed
+forms) equal the oracle's, bit-exactly (SURVEY §4 tier T1)."""
+import os
+import random
+import re
+import subprocess
+
+import pytest
+
+import synth
+from oracle import layout as OL
+from oracle import planner as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "zero_b200.h")
+
+
+@pytest.fixture(scope="module")
+def z():
+    import paper_1910_02054_b200 as z
+    return z
+
+
+def _declared():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:zero_status|uint64_t|const char\*|void|int)\s+(zero_\w+)\s*\(", src, re.M)))
+
+
+def test_exports_every_declared_symbol(z):
+    names = _declared()
+    assert len(names) >= 18
+    from paper_1910_02054_b200.zero import lib, _LIB_PATH, EXPORTS
+    for n in names:
+        assert hasattr(lib, n), n
+    assert sorted(EXPORTS) == names
+    dyn = subprocess.run(["nm", "-D", "--defined-only", _LIB_PATH], capture_output=True, text=True).stdout
+    for n in names:
+        assert re.search(rf"\bT {n}\b", dyn), n
+    assert z.zero.lib.zero_abi_version() == 1
+
+
+def test_library_built_for_sm100a():
+    from paper_1910_02054_b200.zero import _LIB_PATH
+    out = subprocess.run(["cuobjdump", "--list-elf", _LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def _cmp_layout(z, numels, layers, n, a, cb):
+    ol = OL.make_layout(numels, layers, n, a, cb)
+    info, bk, pc = z.plan_layout(numels, layers, n, a, cb)
+    assert info.psi == ol.psi and info.psi_padded == ol.psi_padded and info.shard == ol.shard
+    assert info.n_buckets == len(ol.buckets)
+    got = []
+    for b in bk:
+        ps = [(p.tensor, p.tensor_off, p.bucket_off, p.count) for p in pc[b.first_piece:b.first_piece + b.n_pieces]]
+        got.append((b.layer, b.base, b.size, b.shard_off, ps))
+    want = [(b.layer, b.base, b.size, b.shard_off, [(p.tensor, p.tensor_off, p.bucket_off, p.count) for p in b.pieces])
+            for b in ol.buckets]
+    assert got == want
+
+
+def test_layout_matches_oracle_random(z):
+    rnd = random.Random(99)
+    for _ in range(600):
+        nt = rnd.randint(1, 10)
+        numels = [rnd.choice([0, 1, 5, 63, 64, 65, 127, 1000]) if rnd.random() < 0.5 else rnd.randint(1, 5000)
+                  for _ in range(nt)]
+        if sum(numels) == 0:
+            numels[-1] = 3
+        layers, L = [], 0
+        for _t in range(nt):
+            L += rnd.random() < 0.35
+            layers.append(L)
+        n = rnd.choice([1, 2, 3, 4, 5, 8])
+        a = rnd.choice([1, 2, 8, 64])
+        q = n * a
+        cb = rnd.choice([0, q, 3 * q, rnd.randint(q, 50 * q)])
+        _cmp_layout(z, numels, layers, n, a, cb)
+
+
+@pytest.mark.parametrize("name", ["mlp1m", "gpt2_1.5b", "gpt_7.5b", "gpt_60b"])
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+def test_layout_matches_oracle_paper_models(z, name, n):
+    ts = synth.CONFIGS[name]()
+    cb = (1 << 17) if name == "mlp1m" else (1 << 26)
+    _cmp_layout(z, [t.numel for t in ts], [t.layer for t in ts], n, 64, cb)
+
+
+def test_layout_errors(z):
+    with pytest.raises(z.ZeroError):
+        z.plan_layout([10], [0], 4, 3, 0)          # A not a power of two
+    with pytest.raises(z.ZeroError):
+        z.plan_layout([10], [0], 4, 64, 100)       # C_B < N*A
+    with pytest.raises(z.ZeroError):
+        z.plan_layout([10, 10], [1, 0], 2, 1, 0)   # decreasing layers
+    with pytest.raises(z.ZeroError):
+        z.plan_layout([0], [0], 2, 1, 0)           # no elements
+    with pytest.raises(z.ZeroError):
+        z.plan_layout([10], [0], 9, 1, 0)          # n_d > 8
+
+
+def test_init_argument_errors(z):
+    ts = synth.mlp_layout((9, 4))
+    nl, ll = [t.numel for t in ts], [t.layer for t in ts]
+    from paper_1910_02054_b200.zero import ZeroConfig, ZeroEngine, ZeroError
+    with pytest.raises(ZeroError, match="EINVAL"):
+        ZeroEngine(nl, ll, 2, 0, 1, transport="local", bind=False)             # LOCAL with n_d > 1
+    with pytest.raises(ZeroError, match="EINVAL"):
+        ZeroEngine(nl, ll, 1, 0, 4, bind=False)                               # stage 4
+    with pytest.raises(ZeroError, match="EUNSUPPORTED"):
+        ZeroEngine(nl, ll, 2, 0, 1, ZeroConfig(reduce_mode="R32"), transport="nccl", nccl_comm=1, bind=False)
+    with pytest.raises(ZeroError, match="EINVAL"):
+        ZeroEngine(nl, ll, 1, 0, 1, ZeroConfig(param_dtype="fp16", grad_dtype="bf16"), bind=False)
+    from paper_1910_02054_b200 import zero as zz
+    import ctypes as C
+    d, keep = zz._desc(nl, ll, 64, 0)
+    ctx = C.c_void_p()
+    st = zz.lib.zero_init(C.byref(d), 1, 0, 1, 16, C.byref(ZeroConfig().to_c()), 0, None, None, C.byref(ctx))
+    assert st == 1 and b"K must be 12" in zz.lib.zero_last_error(None)
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+@pytest.mark.parametrize("stage", [0, 1, 2, 3])
+def test_memory_arenas_equal_paper_formulas(z, n, stage):
+    """zero_query(MEMORY) of the 7.5B layout (Fig. 1's model) equals (2+2+K)Psi'... per
+    stage on the padded Psi', exactly; printed at Table 1 precision it
+    gives the paper's DP=1 / DP=4 rows."""
+    from paper_1910_02054_b200.zero import ZeroEngine
+    ts = synth.gpt_7p5b()
+    e = ZeroEngine([t.numel for t in ts], [t.layer for t in ts], n, 0, stage,
+                   transport="local" if n == 1 else "peer", bind=False)
+    m = e.memory()
+    pp = e.info.psi_padded
+    if stage == 0:
+        want = P.model_state_bytes(pp, 12, 1, 0)     # replicated DP holds everything
+    else:
+        want = P.model_state_bytes(pp, 12, n, stage)
+    assert m.params16 + m.grads16 + m.optimizer == want
+    assert m.reduced_grad_extra == 0                  # R16 storage (reading c-8 #21)
+    assert z.model_state_bytes(pp, 12, n, stage) == int(P.model_state_bytes(pp, 12, n, stage))
+    gb = (m.params16 + m.grads16 + m.optimizer) / 1e9
+    printed = {(1, s): 120.0 for s in range(4)}
+    printed.update({(4, 1): 52.5, (4, 2): 41.25, (4, 3): 30.0})
+    if (n, stage) in printed:
+        assert abs(gb - printed[(n, stage)]) / printed[(n, stage)] < 1e-5    # padding < 0.001 %
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+@pytest.mark.parametrize("stage", [0, 1, 2, 3])
+def test_comm_volume_closed_forms(z, n, stage):
+    ts = synth.gpt2_1p5b()
+    info, _, _ = z.plan_layout([t.numel for t in ts], [t.layer for t in ts], n, 64, 1 << 26)
+    got = z.comm_elems_per_rank(info.psi_padded, n, stage)
+    assert got == P.step_elems_per_rank(info.psi_padded, n, stage)
