@@ -74,6 +74,17 @@ def ncu_traffic(kernel: str):
         return None, None
 
 
+def max_over_ranks(value: float, device) -> float:
+    """Max of a per-rank time over all ranks (identity without torch.distributed)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return value
+    t = torch.tensor([value], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.sw_power_cap",
@@ -264,11 +275,7 @@ def main():
     torch.cuda.synchronize()
     clocks.mark(False)
     barrier()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, dev)
     clk = clocks.stop()
     tm = eng.timing()
     gpu_launches = tm.kernel_launches - launches0
@@ -279,7 +286,7 @@ def main():
 
     # roofline of the dominant kernel (fused Adam), measured live with events on its stream
     hbm_peak, peak_kind = peaks()
-    S_e = eng.sizes.opt_bytes // 12
+    S_e = info.psi_padded if args.stage == 0 else info.shard
     g_bytes = 4 if (cfg.reduce_mode == "R32" and world > 1) else 2
     adam_bytes = (24 + g_bytes + 2) * S_e     # p32, m, v read+write, G read, p16 write
     adam_ms = tm.adam_ms / max(tm.steps, 1)
@@ -334,11 +341,7 @@ def main():
             stream.synchronize()    # the host reads the step's result before the next step
         e1.record(stream)
         torch.cuda.synchronize()
-        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
-        if world > 1:
-            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / args.e2e_steps, dev)
         line["e2e"] = {"value": psi_total / (e2e_ms * 1e-3) / 1e9, "unit": "Gparams/s",
                        "h2d_bytes_per_step": int(grad_buf.numel() * grad_buf.element_size()),
                        "d2h_bytes_per_step": 32, "ms_per_step": e2e_ms, "steps": args.e2e_steps}

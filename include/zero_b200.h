@@ -183,7 +183,8 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
                       void* compute_stream, struct zero_ctx** out);
 
 /* Bytes of each arena the caller must allocate (device memory, >= 256-B aligned).
- *  opt     12 * S_e : fp32 master | momentum | variance, S_e elements each
+ *  opt     12 * stride : fp32 master | momentum | variance, S_e elements each at
+ *                     a stride of opt_stride_elems = S_e rounded up to 64
  *                     (S_e = Psi'/N_d; Psi' at stage 0)            -- K Psi / N_d
  *  p16     2 * Psi' (stages 0-2: full replica) or 2 * Psi'/N_d (stage 3 shard)
  *  grad    2 * Psi' (stages 0/1: flat gradient buffer, reduced in place) or
@@ -196,6 +197,7 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
  * allocated during a step (M_D). */
 typedef struct {
   uint64_t opt_bytes, p16_bytes, grad_bytes, gred_bytes, gather_bytes, scratch_bytes;
+  uint64_t opt_stride_elems;   /* element offset of m (and 2x that of v) inside opt */
 } zero_sizes;
 zero_status zero_buffer_sizes(const struct zero_ctx* ctx, zero_sizes* out);
 

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -161,6 +162,7 @@ struct zero_ctx {
   int n_slots = 0;
   std::vector<uint64_t> tensor_flat;               // tensor -> global flat offset of element 0
   uint64_t S_e = 0;                                // elements this rank updates
+  uint64_t opt_stride = 0;                         // S_e rounded up to 64 (256-B aligned m, v)
   uint64_t max_layer = 0;
   uint32_t pool = 2;
 
@@ -182,6 +184,8 @@ struct zero_ctx {
   AdamSeg* segs = nullptr;
   std::vector<AdamSeg> segs_host;
   int sms = 148;
+  int adam_variant = 0;                            // ZERO_ADAM_VARIANT (tuning experiments)
+  int flat_vecs = 2, flat_ctas = 4;                // ZERO_FLAT_VECS / ZERO_FLAT_CTAS
 
   // per-step tracking
   std::vector<uint8_t> reduced;
@@ -478,7 +482,9 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
   // arena sizes (zero_sizes doc in the header)
   const uint64_t P = c->info.psi_padded, S = c->info.shard;
   zero_sizes& z = c->sizes;
-  z.opt_bytes = 12ull * c->S_e;
+  c->opt_stride = align_up(c->S_e, 64);
+  z.opt_bytes = 12ull * c->opt_stride;
+  z.opt_stride_elems = c->opt_stride;
   z.p16_bytes = 2ull * (stage == 3 ? S : P);
   if (stage <= 1) z.grad_bytes = 2ull * P;
   else z.grad_bytes = (n_d > 1) ? 2ull * c->pool * c->maxB : 0;
@@ -518,8 +524,8 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
     return ZERO_EINVAL;
   c->bufs = *b;
   c->p32 = reinterpret_cast<float*>(b->opt);
-  c->m = c->p32 + c->S_e;
-  c->v = c->m + c->S_e;
+  c->m = c->p32 + c->opt_stride;
+  c->v = c->m + c->opt_stride;
   c->p16 = reinterpret_cast<uint16_t*>(b->p16);
   c->grad = reinterpret_cast<uint16_t*>(b->grad);
   c->gred = b->gred;
@@ -534,6 +540,11 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   c->gathered = reinterpret_cast<RankPartial*>(s + sl.gathered);
   c->segs = reinterpret_cast<AdamSeg*>(s + sl.segs);
   c->sms = sm_count();
+  if (const char* ev = getenv("ZERO_ADAM_VARIANT")) c->adam_variant = atoi(ev);
+  if (const char* ev = getenv("ZERO_FLAT_VECS")) c->flat_vecs = atoi(ev);
+  if (const char* ev = getenv("ZERO_FLAT_CTAS")) c->flat_ctas = atoi(ev);
+  if (c->flat_vecs != 1 && c->flat_vecs != 2 && c->flat_vecs != 4 && c->flat_vecs != 8) c->flat_vecs = 2;
+  if (c->flat_ctas < 1 || c->flat_ctas > 8) c->flat_ctas = 4;
 
   // streams and events
   if (c->transport == ZERO_TRANSPORT_NCCL) {
@@ -579,7 +590,7 @@ zero_status zero_load_master(zero_ctx* c, const void* const* tensor_master) {
   if (!tensor_master) return c->fail(ZERO_EINVAL, "tensor_master is NULL");
   for (auto& p : c->pieces)
     if (!tensor_master[p.tensor]) return c->fail(ZERO_EINVAL, "master pointer of tensor %u is NULL", p.tensor);
-  CK(cudaMemsetAsync(c->m, 0, 8ull * c->S_e, c->stream));  // m and v are contiguous
+  CK(cudaMemsetAsync(c->m, 0, 8ull * c->opt_stride, c->stream));  // m and v are contiguous
   for (uint32_t k = 0; k < c->info.n_buckets; ++k) {
     const zero_bucket& b = c->buckets[k];
     const uint64_t sl = b.size / c->n_d;
@@ -645,7 +656,7 @@ zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads) {
         fp.src = nullptr;
       }
       fp.chunk_begin = chunks;
-      chunks += (fp.count + 4095) / 4096;
+      chunks += (fp.count + flat_chunk(c->flat_vecs) - 1) / flat_chunk(c->flat_vecs);
       a.pieces[j - b0] = fp;
     }
     a.n_pieces = (int)(b1 - b0);
@@ -658,7 +669,7 @@ zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads) {
     a.st = c->st;
     a.part = c->part_compute;
     a.slot = c->slots + slot;
-    CK(launch_flatten(a, grid_for(chunks, 4, c->sms), c->stream));
+    CK(launch_flatten(a, grid_for(chunks, c->flat_ctas, c->sms), c->stream, c->flat_vecs));
     c->launches++;
   }
   return ZERO_OK;
@@ -816,7 +827,7 @@ zero_status issue_adam(zero_ctx* c, ZeroGroup* g) {
   a.segs = c->segs;
   a.n_segs = (int)c->segs_host.size();
   a.total = c->S_e;
-  const int grid = grid_for((c->S_e + 2047) / 2048, 2, c->sms);
+  const int grid = grid_for((c->S_e + 2047) / 2048, adam_ctas_per_sm(c->adam_variant), c->sms);
   a.per_cta = align_up((c->S_e + grid - 1) / grid, 8);
   a.beta1 = c->cfg.beta1;
   a.beta2 = c->cfg.beta2;
@@ -826,7 +837,7 @@ zero_status issue_adam(zero_ctx* c, ZeroGroup* g) {
   a.wd = c->cfg.weight_decay > 0.0f ? 1 : 0;
   a.lrwd = (float)((double)c->cfg.lr * (double)c->cfg.weight_decay);
   a.st = c->st;
-  CK(launch_adam(a, grid, c->comm_stream));
+  CK(launch_adam(a, grid, c->comm_stream, c->adam_variant));
   c->launches++;
   c->adam_launches++;
   return ZERO_OK;
@@ -1112,7 +1123,7 @@ zero_status zero_query(const zero_ctx* cc, int what, void* out, size_t n) {
       const zero_sizes& z = c->sizes;
       const uint64_t S = c->info.shard;
       mem.params16 = z.p16_bytes;
-      mem.optimizer = z.opt_bytes;
+      mem.optimizer = 12ull * c->S_e;                  // logical K*S_e (the arena may pad m, v to 64)
       if (c->stage <= 1) {
         mem.grads16 = z.grad_bytes;
         mem.reduced_grad_extra = z.gred_bytes;

@@ -135,7 +135,7 @@ __device__ void grid_publish(double s, uint32_t f, GridPartials* part, Slot* slo
 // ---------------------------------------------------------------------------
 // K2: flatten / cast / prescale one gradient bucket (a1), + epilogue at N_d = 1
 // ---------------------------------------------------------------------------
-constexpr int kFlatChunk = 4096;  // elements per chunk = 256 threads x 2 x 8
+// chunk = 256 threads x V vectors x 8 elements; V is a template parameter
 
 template <int SDT>
 struct SrcLoad;
@@ -175,8 +175,9 @@ struct SrcLoad<DT_F32> {
 };
 
 // g' = RTNE16(widen(g) * sigma): a plain bit copy when sigma == 1 and the dtypes match
-template <int SDT, int DDT, bool kCopy>
+template <int SDT, int DDT, bool kCopy, int V>
 __global__ void __launch_bounds__(kThreads) k_flatten(const __grid_constant__ FlatArgs a) {
+  constexpr uint32_t kFlatChunk = kThreads * 8 * V;
   using S = SrcLoad<SDT>;
   using D = H16<DDT>;
   const float sigma = a.sigma;
@@ -230,17 +231,19 @@ __global__ void __launch_bounds__(kThreads) k_flatten(const __grid_constant__ Fl
       st128(dst + i, o);
     };
     if (vec) {
-#pragma unroll 1
-      for (uint32_t i0 = threadIdx.x * 8; i0 < n; i0 += kThreads * 16) {
-        const uint32_t i1 = i0 + kThreads * 8;
-        float x0[8], x1[8];
-        const bool f0 = i0 + 8 <= n, f1 = i1 + 8 <= n;
-        if (f0) S::vec(src + (uint64_t)i0 * S::kBytes, x0);
-        if (f1) S::vec(src + (uint64_t)i1 * S::kBytes, x1);
-        if (f0) emit8(i0, x0);
-        else for (uint32_t j = i0; j < n; ++j) emit_one(j);
-        if (f1) emit8(i1, x1);
-        else for (uint32_t j = i1; j < n; ++j) emit_one(j);
+      float x[V][8];
+      bool full[V];
+#pragma unroll
+      for (int u = 0; u < V; ++u) {
+        const uint32_t i = threadIdx.x * 8 + u * kThreads * 8;
+        full[u] = i + 8 <= n;
+        if (full[u]) S::vec(src + (uint64_t)i * S::kBytes, x[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < V; ++u) {
+        const uint32_t i = threadIdx.x * 8 + u * kThreads * 8;
+        if (full[u]) emit8(i, x[u]);
+        else for (uint32_t j = i; j < n; ++j) emit_one(j);
       }
     } else {
       for (uint32_t j = threadIdx.x; j < n; j += kThreads) emit_one(j);
@@ -249,9 +252,10 @@ __global__ void __launch_bounds__(kThreads) k_flatten(const __grid_constant__ Fl
   if (a.epilogue) grid_publish(sumsq, flag, a.part, a.slot);
 }
 
-cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s) {
+template <int V>
+cudaError_t launch_flatten_v(const FlatArgs& a, int grid, cudaStream_t s) {
   const bool copy = (a.sigma == 1.0f) && (a.src_dtype == a.dst_dtype);
-#define ZL(SD, DD, CP) k_flatten<SD, DD, CP><<<grid, kThreads, 0, s>>>(a)
+#define ZL(SD, DD, CP) k_flatten<SD, DD, CP, V><<<grid, kThreads, 0, s>>>(a)
   if (a.dst_dtype == DT_F16) {
     if (a.src_dtype == DT_F16) { if (copy) ZL(DT_F16, DT_F16, true); else ZL(DT_F16, DT_F16, false); }
     else if (a.src_dtype == DT_F32) ZL(DT_F32, DT_F16, false);
@@ -265,6 +269,17 @@ cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s) {
   }
 #undef ZL
   return cudaGetLastError();
+}
+
+uint32_t flat_chunk(int vecs) { return (uint32_t)kThreads * 8u * (uint32_t)vecs; }
+
+cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s, int vecs) {
+  switch (vecs) {
+    case 1: return launch_flatten_v<1>(a, grid, s);
+    case 4: return launch_flatten_v<4>(a, grid, s);
+    case 8: return launch_flatten_v<8>(a, grid, s);
+    default: return launch_flatten_v<2>(a, grid, s);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -492,8 +507,31 @@ __device__ __forceinline__ void adam_elem(float& p, float& m, float& v, float G,
 }
 
 template <int PDT, int GDT>
-__global__ void __launch_bounds__(kThreads, 2) k_adam(const __grid_constant__ AdamArgs a) {
+struct AdamIO {
   using P = H16<PDT>;
+  static __device__ __forceinline__ void load_g(const void* G, uint64_t idx, float (&g)[8]) {
+    if (GDT == DT_F32) {
+      U8 w = ld256(reinterpret_cast<const float*>(G) + idx);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g[j] = __uint_as_float(w.x[j]);
+    } else {
+      U4 w = ld128(reinterpret_cast<const uint16_t*>(G) + idx);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g[j] = H16<GDT == DT_F32 ? DT_F16 : GDT>::widen(h_get(w, j));
+    }
+  }
+  static __device__ __forceinline__ float load_g1(const void* G, uint64_t idx) {
+    if (GDT == DT_F32) return reinterpret_cast<const float*>(G)[idx];
+    return H16<GDT == DT_F32 ? DT_F16 : GDT>::widen(reinterpret_cast<const uint16_t*>(G)[idx]);
+  }
+};
+
+// MINB: CTAs per SM the register budget is sized for; U: 8-element groups per
+// thread per iteration (all loads of an iteration are issued before any math).
+template <int PDT, int GDT, int MINB, int U>
+__global__ void __launch_bounds__(kThreads, MINB) k_adam(const __grid_constant__ AdamArgs a) {
+  using P = H16<PDT>;
+  using IO = AdamIO<PDT, GDT>;
   if (a.st->skip) return;  // overflow: the whole step is skipped (reading c-4)
   AdamScalars c;
   c.inv = a.st->inv_adam;
@@ -527,41 +565,44 @@ __global__ void __launch_bounds__(kThreads, 2) k_adam(const __grid_constant__ Ad
     if (((cur | (uint64_t)gd | (uint64_t)pd) & 7) == 0) {
       vend = cur + ((send - cur) & ~(uint64_t)7);
 #pragma unroll 1
-      for (uint64_t i = cur + threadIdx.x * 8; i < vend; i += kThreads * 8) {
-        U8 p = ld256(a.p32 + i);
-        U8 m = ld256(a.m + i);
-        U8 v = ld256(a.v + i);
-        float G[8];
-        if (GDT == DT_F32) {
-          U8 g = ld256(reinterpret_cast<const float*>(a.G) + (i + gd));
+      for (uint64_t i0 = cur + threadIdx.x * 8; i0 < vend; i0 += (uint64_t)kThreads * 8 * U) {
+        U8 p[U], m[U], v[U];
+        float G[U][8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) G[j] = __uint_as_float(g.x[j]);
-        } else {
-          U4 g = ld128(reinterpret_cast<const uint16_t*>(a.G) + (i + gd));
-#pragma unroll
-          for (int j = 0; j < 8; ++j) G[j] = H16<GDT == DT_F32 ? DT_F16 : GDT>::widen(h_get(g, j));
+        for (int u = 0; u < U; ++u) {
+          const uint64_t i = i0 + (uint64_t)u * kThreads * 8;
+          if (u == 0 || i < vend) {
+            p[u] = ld256(a.p32 + i);
+            m[u] = ld256(a.m + i);
+            v[u] = ld256(a.v + i);
+            IO::load_g(a.G, i + gd, G[u]);
+          }
         }
-        U4 o;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float pj = __uint_as_float(p.x[j]), mj = __uint_as_float(m.x[j]), vj = __uint_as_float(v.x[j]);
-          adam_elem(pj, mj, vj, G[j], c);
-          p.x[j] = __float_as_uint(pj);
-          m.x[j] = __float_as_uint(mj);
-          v.x[j] = __float_as_uint(vj);
-          h_set(o, j, P::narrow(pj));
+        for (int u = 0; u < U; ++u) {
+          const uint64_t i = i0 + (uint64_t)u * kThreads * 8;
+          if (u == 0 || i < vend) {
+            U4 o;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float pj = __uint_as_float(p[u].x[j]), mj = __uint_as_float(m[u].x[j]), vj = __uint_as_float(v[u].x[j]);
+              adam_elem(pj, mj, vj, G[u][j], c);
+              p[u].x[j] = __float_as_uint(pj);
+              m[u].x[j] = __float_as_uint(mj);
+              v[u].x[j] = __float_as_uint(vj);
+              h_set(o, j, P::narrow(pj));
+            }
+            st256(a.p32 + i, p[u]);
+            st256(a.m + i, m[u]);
+            st256(a.v + i, v[u]);
+            for (int d = 0; d < a.n_p16; ++d) st128(reinterpret_cast<uint16_t*>(a.p16[d]) + (i + pd), o);
+          }
         }
-        st256(a.p32 + i, p);
-        st256(a.m + i, m);
-        st256(a.v + i, v);
-        for (int d = 0; d < a.n_p16; ++d) st128(reinterpret_cast<uint16_t*>(a.p16[d]) + (i + pd), o);
       }
     }
     for (uint64_t i = vend + threadIdx.x; i < send; i += kThreads) {  // unaligned remainder
       float p = a.p32[i], m = a.m[i], v = a.v[i];
-      float G;
-      if (GDT == DT_F32) G = reinterpret_cast<const float*>(a.G)[i + gd];
-      else G = H16<GDT == DT_F32 ? DT_F16 : GDT>::widen(reinterpret_cast<const uint16_t*>(a.G)[i + gd]);
+      const float G = IO::load_g1(a.G, i + gd);
       adam_elem(p, m, v, G, c);
       a.p32[i] = p;
       a.m[i] = m;
@@ -573,21 +614,37 @@ __global__ void __launch_bounds__(kThreads, 2) k_adam(const __grid_constant__ Ad
   }
 }
 
-cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s) {
-#define ZA(PD, GD) k_adam<PD, GD><<<grid, kThreads, 0, s>>>(a)
-  if (a.p_dtype == DT_F16) {
-    if (a.g_dtype == DT_F16) ZA(DT_F16, DT_F16);
-    else if (a.g_dtype == DT_F32) ZA(DT_F16, DT_F32);
-    else return cudaErrorInvalidValue;
-  } else if (a.p_dtype == DT_BF16) {
-    if (a.g_dtype == DT_BF16) ZA(DT_BF16, DT_BF16);
-    else if (a.g_dtype == DT_F32) ZA(DT_BF16, DT_F32);
-    else return cudaErrorInvalidValue;
-  } else {
-    return cudaErrorInvalidValue;
+// variants: 0 = (2 CTAs/SM, U=1), 1 = (4, 1), 2 = (2, 2), 3 = (3, 1), 4 = (1, 4)
+int adam_ctas_per_sm(int variant) {
+  switch (variant) {
+    case 1: return 4;
+    case 3: return 3;
+    case 4: return 1;
+    default: return 2;
   }
-#undef ZA
+}
+
+template <int PD, int GD>
+cudaError_t launch_adam_t(const AdamArgs& a, int grid, cudaStream_t s, int variant) {
+  switch (variant) {
+    case 1: k_adam<PD, GD, 4, 1><<<grid, kThreads, 0, s>>>(a); break;
+    case 2: k_adam<PD, GD, 2, 2><<<grid, kThreads, 0, s>>>(a); break;
+    case 3: k_adam<PD, GD, 3, 1><<<grid, kThreads, 0, s>>>(a); break;
+    case 4: k_adam<PD, GD, 1, 4><<<grid, kThreads, 0, s>>>(a); break;
+    default: k_adam<PD, GD, 2, 1><<<grid, kThreads, 0, s>>>(a); break;
+  }
   return cudaGetLastError();
+}
+
+cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int variant) {
+  if (a.p_dtype == DT_F16) {
+    if (a.g_dtype == DT_F16) return launch_adam_t<DT_F16, DT_F16>(a, grid, s, variant);
+    if (a.g_dtype == DT_F32) return launch_adam_t<DT_F16, DT_F32>(a, grid, s, variant);
+  } else if (a.p_dtype == DT_BF16) {
+    if (a.g_dtype == DT_BF16) return launch_adam_t<DT_BF16, DT_BF16>(a, grid, s, variant);
+    if (a.g_dtype == DT_F32) return launch_adam_t<DT_BF16, DT_F32>(a, grid, s, variant);
+  }
+  return cudaErrorInvalidValue;
 }
 
 // ---------------------------------------------------------------------------

@@ -135,12 +135,14 @@ struct LoadArgs {             // master init: fp32 piece -> shard / 16-bit copy
 };
 
 // launchers (kernels.cu); return the launch error
-cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s, int vecs);
+uint32_t flat_chunk(int vecs);
 cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_decide_local(const Slot* slots, int n_slots, RankPartial* out, cudaStream_t s);
 struct PartialPtrs { const RankPartial* p[kMaxRanks]; };
 cudaError_t launch_decide_global(const PartialPtrs& partials, DevState* st, DecideParams p, cudaStream_t s);
-cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int variant);
+int adam_ctas_per_sm(int variant);
 cudaError_t launch_copy(const CopyArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_load(const LoadArgs& a, cudaStream_t s);
 cudaError_t launch_init_state(DevState* st, float S, float inv, cudaStream_t s);

@@ -70,7 +70,7 @@ class CStepInfo(C.Structure):
 
 class CSizes(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("opt_bytes", "p16_bytes", "grad_bytes", "gred_bytes",
-                                          "gather_bytes", "scratch_bytes")]
+                                          "gather_bytes", "scratch_bytes", "opt_stride_elems")]
 
 
 class CBuffers(C.Structure):
@@ -347,10 +347,11 @@ class ZeroEngine:
 
     # -- arena views (for tests and checkpointing) -----------------------------
     def shard(self):
-        """(p32, m, v) fp32 views of this rank's optimizer arena."""
+        """(p32, m, v) fp32 views of this rank's optimizer arena (S_e elements each)."""
         o = self.arenas["opt"].view(torch.float32)
-        s = o.numel() // 3
-        return o[:s], o[s:2 * s], o[2 * s:]
+        st = self.sizes.opt_stride_elems
+        n = self.info.psi_padded if self.stage == 0 else self.info.shard
+        return o[:n], o[st:st + n], o[2 * st:2 * st + n]
 
     def p16_arena(self) -> torch.Tensor:
         return self.arenas["p16"].view(_TORCH_DT[self.config.param_dtype])

@@ -1,0 +1,28 @@
+"""Tuning sweep (GPU): run bench.py under each kernel variant and print the phase times."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+variants = []
+for av in (0, 1, 2, 3, 4):
+    variants.append({"ZERO_ADAM_VARIANT": str(av)})
+for fv in (1, 2, 4, 8):
+    for fc in (2, 4, 8):
+        variants.append({"ZERO_FLAT_VECS": str(fv), "ZERO_FLAT_CTAS": str(fc)})
+extra = sys.argv[1:]
+for v in variants:
+    env = dict(os.environ, **v)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "30", "--no-e2e",
+                        "--no-cpu-baseline"] + extra, env=env, capture_output=True, text=True, timeout=600)
+    try:
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+        print(json.dumps({"variant": v, "ms_per_step": round(d["ms_per_step"], 4),
+                          "adam_ms": round(d["roofline"]["ms_per_launch"], 4),
+                          "adam_frac": round(d["roofline"]["frac"], 4),
+                          "reduce_ms": round(d["step_roofline"]["reduce_phase_ms"], 4),
+                          "flatten_gbs": round(d["step_roofline"]["flatten_gbs"] or 0, 1),
+                          "clocks": d["clocks"]}), flush=True)
+    except Exception as e:
+        print(json.dumps({"variant": v, "error": str(e), "stderr": r.stderr[-2000:]}), flush=True)
