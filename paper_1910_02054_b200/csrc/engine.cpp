@@ -158,6 +158,7 @@ struct zero_ctx {
   std::map<uint32_t, int> layer_index;
   std::vector<std::vector<FlatPiece>> flat_tmpl;   // per bucket: data + zero pieces (src = tensor id)
   std::vector<std::vector<uint32_t>> flat_tensor;  // per bucket: tensor id per flat piece (UINT32_MAX = zero)
+  std::vector<std::vector<uint64_t>> flat_toff;    // per bucket: tensor offset per flat piece
   std::vector<int> slot_base;                      // per bucket: first epilogue slot
   int n_slots = 0;
   std::vector<uint64_t> tensor_flat;               // tensor -> global flat offset of element 0
@@ -183,9 +184,10 @@ struct zero_ctx {
   RankPartial* gathered = nullptr;
   AdamSeg* segs = nullptr;
   std::vector<AdamSeg> segs_host;
+  bool segs_aligned8 = true;                       // every segment offset/count % 8 == 0
   int sms = 148;
   int adam_variant = 0;                            // ZERO_ADAM_VARIANT (tuning experiments)
-  int flat_vecs = 2, flat_ctas = 4;                // ZERO_FLAT_VECS / ZERO_FLAT_CTAS
+  int flat_vecs = 4, flat_ctas = 4;                // ZERO_FLAT_VECS / ZERO_FLAT_CTAS
 
   // per-step tracking
   std::vector<uint8_t> reduced;
@@ -432,6 +434,7 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
   // flatten templates: data pieces + zero pieces covering [0, B_k) exactly
   c->flat_tmpl.resize(c->info.n_buckets);
   c->flat_tensor.resize(c->info.n_buckets);
+  c->flat_toff.resize(c->info.n_buckets);
   c->slot_base.resize(c->info.n_buckets);
   int slots = 0;
   for (uint32_t k = 0; k < c->info.n_buckets; ++k) {
@@ -442,9 +445,9 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
       fp.src = tensor_tag;
       fp.dst_off = off;
       fp.count = n;
-      fp.chunk_begin = toff;  // holds tensor_off until the launch fills src/chunks
       c->flat_tmpl[k].push_back(fp);
       c->flat_tensor[k].push_back(tensor);
+      c->flat_toff[k].push_back(toff);
     };
     for (uint32_t j = 0; j < b.n_pieces; ++j) {
       const zero_piece& p = c->pieces[b.first_piece + j];
@@ -477,6 +480,7 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
       s.p16_off = stage == 3 ? b.shard_off : mine;
     }
     c->segs_host.push_back(s);
+    if ((s.local_off | s.g_off | s.p16_off | s.count) & 7) c->segs_aligned8 = false;
   }
 
   // arena sizes (zero_sizes doc in the header)
@@ -543,7 +547,7 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   if (const char* ev = getenv("ZERO_ADAM_VARIANT")) c->adam_variant = atoi(ev);
   if (const char* ev = getenv("ZERO_FLAT_VECS")) c->flat_vecs = atoi(ev);
   if (const char* ev = getenv("ZERO_FLAT_CTAS")) c->flat_ctas = atoi(ev);
-  if (c->flat_vecs != 1 && c->flat_vecs != 2 && c->flat_vecs != 4 && c->flat_vecs != 8) c->flat_vecs = 2;
+  if (c->flat_vecs != 1 && c->flat_vecs != 2 && c->flat_vecs != 4 && c->flat_vecs != 8) c->flat_vecs = 4;
   if (c->flat_ctas < 1 || c->flat_ctas > 8) c->flat_ctas = 4;
 
   // streams and events
@@ -644,32 +648,31 @@ zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads) {
   for (size_t b0 = 0; b0 < tmpl.size(); b0 += kMaxFlatPieces, ++slot) {
     FlatArgs a{};
     const size_t b1 = std::min(tmpl.size(), b0 + kMaxFlatPieces);
-    uint64_t chunks = 0;
     for (size_t j = b0; j < b1; ++j) {
       FlatPiece fp = tmpl[j];
       const uint32_t t = c->flat_tensor[k][j];
       if (t != UINT32_MAX) {
         const char* base = reinterpret_cast<const char*>(grads[t]);
         if (!base) return c->fail(ZERO_EINVAL, "gradient pointer of tensor %u is NULL", t);
-        fp.src = base + fp.chunk_begin * ebytes;  // chunk_begin held tensor_off
+        fp.src = base + c->flat_toff[k][j] * ebytes;
       } else {
         fp.src = nullptr;
       }
-      fp.chunk_begin = chunks;
-      chunks += (fp.count + flat_chunk(c->flat_vecs) - 1) / flat_chunk(c->flat_vecs);
       a.pieces[j - b0] = fp;
     }
     a.n_pieces = (int)(b1 - b0);
+    const uint64_t total = tmpl[b1 - 1].dst_off + tmpl[b1 - 1].count - tmpl[b0].dst_off;
+    const int grid = grid_for((total + 2047) / 2048, c->flat_ctas, c->sms);
+    a.per_cta = align_up((total + grid - 1) / grid, 8);
     a.src_dtype = c->gdt;
     a.dst_dtype = c->pdt;
     a.epilogue = epi ? 1 : 0;
-    a.total_chunks = chunks;
     a.dst = dst;
     a.sigma = c->cfg.grad_prescale;
     a.st = c->st;
     a.part = c->part_compute;
     a.slot = c->slots + slot;
-    CK(launch_flatten(a, grid_for(chunks, c->flat_ctas, c->sms), c->stream, c->flat_vecs));
+    CK(launch_flatten(a, grid, c->stream, c->flat_vecs));
     c->launches++;
   }
   return ZERO_OK;
@@ -827,7 +830,9 @@ zero_status issue_adam(zero_ctx* c, ZeroGroup* g) {
   a.segs = c->segs;
   a.n_segs = (int)c->segs_host.size();
   a.total = c->S_e;
-  const int grid = grid_for((c->S_e + 2047) / 2048, adam_ctas_per_sm(c->adam_variant), c->sms);
+  int variant = c->adam_variant;
+  if (adam_variant_is_tma(variant) && !c->segs_aligned8) variant = 0;  // bulk copies need 16-B granules
+  const int grid = grid_for((c->S_e + 2047) / 2048, adam_ctas_per_sm(variant), c->sms);
   a.per_cta = align_up((c->S_e + grid - 1) / grid, 8);
   a.beta1 = c->cfg.beta1;
   a.beta2 = c->cfg.beta2;
@@ -837,7 +842,7 @@ zero_status issue_adam(zero_ctx* c, ZeroGroup* g) {
   a.wd = c->cfg.weight_decay > 0.0f ? 1 : 0;
   a.lrwd = (float)((double)c->cfg.lr * (double)c->cfg.weight_decay);
   a.st = c->st;
-  CK(launch_adam(a, grid, c->comm_stream, c->adam_variant));
+  CK(launch_adam(a, grid, c->comm_stream, variant));
   c->launches++;
   c->adam_launches++;
   return ZERO_OK;

@@ -174,10 +174,13 @@ struct SrcLoad<DT_F32> {
   static __device__ __forceinline__ float one(const void* p, uint64_t i) { return reinterpret_cast<const float*>(p)[i]; }
 };
 
-// g' = RTNE16(widen(g) * sigma): a plain bit copy when sigma == 1 and the dtypes match
+// g' = RTNE16(widen(g) * sigma): a plain bit copy when sigma == 1 and the dtypes match.
+// The pieces tile the destination range [pieces[0].dst_off, last end) contiguously
+// (data pieces and zero pieces for alignment gaps / padding).  CTA b handles the
+// contiguous slice [b*per_cta, (b+1)*per_cta) of that range, walking the pieces it
+// overlaps; each thread keeps V 128-bit loads in flight.
 template <int SDT, int DDT, bool kCopy, int V>
 __global__ void __launch_bounds__(kThreads) k_flatten(const __grid_constant__ FlatArgs a) {
-  constexpr uint32_t kFlatChunk = kThreads * 8 * V;
   using S = SrcLoad<SDT>;
   using D = H16<DDT>;
   const float sigma = a.sigma;
@@ -185,14 +188,18 @@ __global__ void __launch_bounds__(kThreads) k_flatten(const __grid_constant__ Fl
   double sumsq = 0.0;
   uint32_t flag = 0;
   uint16_t* dst_base = reinterpret_cast<uint16_t*>(a.dst);
-  for (uint64_t c = blockIdx.x; c < a.total_chunks; c += gridDim.x) {
-    int p = 0;
-    while (p + 1 < a.n_pieces && a.pieces[p + 1].chunk_begin <= c) ++p;
+  const uint64_t r0 = a.pieces[0].dst_off;
+  const uint64_t r1 = a.pieces[a.n_pieces - 1].dst_off + a.pieces[a.n_pieces - 1].count;
+  const uint64_t lo = r0 + (uint64_t)blockIdx.x * a.per_cta;
+  const uint64_t hi = lo + a.per_cta < r1 ? lo + a.per_cta : r1;
+  int p = 0;
+  while (p + 1 < a.n_pieces && a.pieces[p + 1].dst_off <= lo) ++p;
+  for (uint64_t cur = lo; cur < hi && p < a.n_pieces; ++p) {
     const FlatPiece pc = a.pieces[p];
-    const uint64_t e0 = (c - pc.chunk_begin) * (uint64_t)kFlatChunk;
-    const uint64_t rem = pc.count - e0;
-    const uint32_t n = rem < (uint64_t)kFlatChunk ? (uint32_t)rem : (uint32_t)kFlatChunk;
-    uint16_t* dst = dst_base + pc.dst_off + e0;
+    const uint64_t pend = pc.dst_off + pc.count < hi ? pc.dst_off + pc.count : hi;
+    if (pend <= cur) continue;
+    uint16_t* dst = dst_base + cur;                       // element 0 of this run
+    const uint32_t n = (uint32_t)(pend - cur);
     if (pc.src == nullptr) {  // alignment gap or bucket padding: zeros (reading c-7)
       if (aligned(dst, 16)) {
         for (uint32_t i = threadIdx.x * 8; i < n; i += kThreads * 8) {
@@ -202,9 +209,10 @@ __global__ void __launch_bounds__(kThreads) k_flatten(const __grid_constant__ Fl
       } else {
         for (uint32_t i = threadIdx.x; i < n; i += kThreads) dst[i] = 0;
       }
+      cur = pend;
       continue;
     }
-    const char* src = reinterpret_cast<const char*>(pc.src) + e0 * S::kBytes;
+    const char* src = reinterpret_cast<const char*>(pc.src) + (cur - pc.dst_off) * S::kBytes;
     const bool vec = aligned(src, 8 * S::kBytes) && aligned(dst, 16);
     auto emit_one = [&](uint32_t j) {
       const float xv = S::one(src, j);
@@ -231,23 +239,26 @@ __global__ void __launch_bounds__(kThreads) k_flatten(const __grid_constant__ Fl
       st128(dst + i, o);
     };
     if (vec) {
-      float x[V][8];
-      bool full[V];
+      const uint32_t nv = n & ~7u;
+#pragma unroll 1
+      for (uint32_t i0 = threadIdx.x * 8; i0 < nv; i0 += kThreads * 8 * V) {
+        float x[V][8];
 #pragma unroll
-      for (int u = 0; u < V; ++u) {
-        const uint32_t i = threadIdx.x * 8 + u * kThreads * 8;
-        full[u] = i + 8 <= n;
-        if (full[u]) S::vec(src + (uint64_t)i * S::kBytes, x[u]);
-      }
+        for (int u = 0; u < V; ++u) {
+          const uint32_t i = i0 + u * kThreads * 8;
+          if (u == 0 || i < nv) S::vec(src + (uint64_t)i * S::kBytes, x[u]);
+        }
 #pragma unroll
-      for (int u = 0; u < V; ++u) {
-        const uint32_t i = threadIdx.x * 8 + u * kThreads * 8;
-        if (full[u]) emit8(i, x[u]);
-        else for (uint32_t j = i; j < n; ++j) emit_one(j);
+        for (int u = 0; u < V; ++u) {
+          const uint32_t i = i0 + u * kThreads * 8;
+          if (u == 0 || i < nv) emit8(i, x[u]);
+        }
       }
+      for (uint32_t j = nv + threadIdx.x; j < n; j += kThreads) emit_one(j);
     } else {
       for (uint32_t j = threadIdx.x; j < n; j += kThreads) emit_one(j);
     }
+    cur = pend;
   }
   if (a.epilogue) grid_publish(sumsq, flag, a.part, a.slot);
 }
@@ -271,7 +282,6 @@ cudaError_t launch_flatten_v(const FlatArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-uint32_t flat_chunk(int vecs) { return (uint32_t)kThreads * 8u * (uint32_t)vecs; }
 
 cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s, int vecs) {
   switch (vecs) {
@@ -614,19 +624,249 @@ __global__ void __launch_bounds__(kThreads, MINB) k_adam(const __grid_constant__
   }
 }
 
-// variants: 0 = (2 CTAs/SM, U=1), 1 = (4, 1), 2 = (2, 2), 3 = (3, 1), 4 = (1, 4)
+// ---------------------------------------------------------------------------
+// a5 (TMA variant): the same fused Adam, with the four input streams staged into
+// shared memory by 1-D bulk copies (cp.async.bulk, the TMA engine) in a
+// STAGES-deep mbarrier ring.  One producer warp keeps up to STAGES tiles of
+// T elements in flight per CTA (decoupled from the math), eight consumer warps
+// compute from shared memory and store p32/m/v/p16 with 256/128-bit STG.
+// Requires every segment offset and count to be a multiple of 8 (host checks).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void lds128(const void* p, uint32_t (&r)[4]) {
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(smem_u32(p)));
+}
+
+// tile iterator over the CTA's contiguous range, split at segment boundaries
+struct TileCursor {
+  uint64_t cur, hi;
+  int s;
+  __device__ __forceinline__ bool next(const AdamArgs& a, uint32_t T, uint64_t& start, uint32_t& n, int64_t& gd,
+                                       int64_t& pd) {
+    while (cur < hi && s < a.n_segs) {
+      const AdamSeg sg = a.segs[s];
+      const uint64_t send = sg.local_off + sg.count < hi ? sg.local_off + sg.count : hi;
+      if (cur >= send) { ++s; continue; }
+      start = cur;
+      const uint64_t left = send - cur;
+      n = left < T ? (uint32_t)left : T;
+      gd = (int64_t)sg.g_off - (int64_t)sg.local_off;
+      pd = (int64_t)sg.p16_off - (int64_t)sg.local_off;
+      cur += n;
+      return true;
+    }
+    return false;
+  }
+};
+
+template <int PDT, int GDT, int T, int STAGES>
+__global__ void __launch_bounds__(T / 8 + 32, 1) k_adam_tma(const __grid_constant__ AdamArgs a) {
+  constexpr int kCons = T / 8;  // consumer threads: 8 elements of every tile each
+  using P = H16<PDT>;
+  constexpr int GB = (GDT == DT_F32) ? 4 : 2;
+  constexpr uint32_t kStageBytes = (uint32_t)T * (12 + GB);
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  uint64_t* empty = full + STAGES;
+  if (a.st->skip) return;  // overflow: skip the step (reading c-4)
+  const uint64_t lo = (uint64_t)blockIdx.x * a.per_cta;
+  if (lo >= a.total) return;
+  const uint64_t hi = lo + a.per_cta < a.total ? lo + a.per_cta : a.total;
+  int s0 = 0, s1 = a.n_segs - 1;
+  while (s0 < s1) {
+    const int mid = (s0 + s1 + 1) >> 1;
+    if (a.segs[mid].local_off <= lo) s0 = mid; else s1 = mid - 1;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kCons / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kCons / 32) {  // ---- producer warp
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      TileCursor tc{lo, hi, s0};
+      uint64_t start;
+      uint32_t n;
+      int64_t gd, pd;
+      for (uint32_t it = 0; tc.next(a, T, start, n, gd, pd); ++it) {
+        const int st = it % STAGES;
+        if (it >= (uint32_t)STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
+        unsigned char* base = smem + st * kStageBytes;
+        mbar_expect_tx(&full[st], n * (12u + GB));
+        bulk_g2s(base, a.p32 + start, n * 4u, &full[st], pol);
+        bulk_g2s(base + T * 4, a.m + start, n * 4u, &full[st], pol);
+        bulk_g2s(base + T * 8, a.v + start, n * 4u, &full[st], pol);
+        bulk_g2s(base + T * 12, reinterpret_cast<const unsigned char*>(a.G) + (start + gd) * GB, n * (uint32_t)GB,
+                 &full[st], pol);
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warps
+  AdamScalars c;
+  c.inv = a.st->inv_adam;
+  c.step = a.st->step_f;
+  c.rsb2 = a.st->rsb2_f;
+  c.clip = a.st->clip_f;
+  c.beta1 = a.beta1;
+  c.beta2 = a.beta2;
+  c.eps = a.eps;
+  c.omb1 = a.omb1;
+  c.omb2 = a.omb2;
+  c.lrwd = a.lrwd;
+  c.wd = a.wd;
+  TileCursor tc{lo, hi, s0};
+  uint64_t start;
+  uint32_t n;
+  int64_t gd, pd;
+  for (uint32_t it = 0; tc.next(a, T, start, n, gd, pd); ++it) {
+    const int st = it % STAGES;
+    mbar_wait(&full[st], (it / STAGES) & 1);
+    const unsigned char* base = smem + st * kStageBytes;
+    {
+      const uint32_t e = threadIdx.x * 8;
+      if (e < n) {
+        U8 p, m, v;
+        float G[8];
+        {
+          uint32_t r[4];
+          lds128(base + e * 4, r);
+          p.x[0] = r[0]; p.x[1] = r[1]; p.x[2] = r[2]; p.x[3] = r[3];
+          lds128(base + e * 4 + 16, r);
+          p.x[4] = r[0]; p.x[5] = r[1]; p.x[6] = r[2]; p.x[7] = r[3];
+          lds128(base + T * 4 + e * 4, r);
+          m.x[0] = r[0]; m.x[1] = r[1]; m.x[2] = r[2]; m.x[3] = r[3];
+          lds128(base + T * 4 + e * 4 + 16, r);
+          m.x[4] = r[0]; m.x[5] = r[1]; m.x[6] = r[2]; m.x[7] = r[3];
+          lds128(base + T * 8 + e * 4, r);
+          v.x[0] = r[0]; v.x[1] = r[1]; v.x[2] = r[2]; v.x[3] = r[3];
+          lds128(base + T * 8 + e * 4 + 16, r);
+          v.x[4] = r[0]; v.x[5] = r[1]; v.x[6] = r[2]; v.x[7] = r[3];
+          if (GB == 4) {
+            lds128(base + T * 12 + e * 4, r);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) G[j] = __uint_as_float(r[j]);
+            lds128(base + T * 12 + e * 4 + 16, r);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) G[4 + j] = __uint_as_float(r[j]);
+          } else {
+            lds128(base + T * 12 + e * 2, r);
+            U4 g{{r[0], r[1], r[2], r[3]}};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) G[j] = H16<GDT == DT_F32 ? DT_F16 : GDT>::widen(h_get(g, j));
+          }
+        }
+        U4 o;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float pj = __uint_as_float(p.x[j]), mj = __uint_as_float(m.x[j]), vj = __uint_as_float(v.x[j]);
+          adam_elem(pj, mj, vj, G[j], c);
+          p.x[j] = __float_as_uint(pj);
+          m.x[j] = __float_as_uint(mj);
+          v.x[j] = __float_as_uint(vj);
+          h_set(o, j, P::narrow(pj));
+        }
+        const uint64_t i = start + e;
+        st256(a.p32 + i, p);
+        st256(a.m + i, m);
+        st256(a.v + i, v);
+        for (int d = 0; d < a.n_p16; ++d) st128(reinterpret_cast<uint16_t*>(a.p16[d]) + (i + pd), o);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+}
+
+template <int PD, int GD, int T, int STAGES>
+cudaError_t launch_adam_tma_t(const AdamArgs& a, int grid, cudaStream_t s) {
+  constexpr int GB = (GD == DT_F32) ? 4 : 2;
+  const size_t smem = (size_t)STAGES * T * (12 + GB) + 2 * STAGES * sizeof(uint64_t);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_adam_tma<PD, GD, T, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k_adam_tma<PD, GD, T, STAGES><<<grid, T / 8 + 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+// variants: 0 = (2 CTAs/SM, U=1), 1 = (4, 1), 2 = (2, 2), 3 = (3, 1), 4 = (1, 4),
+// TMA (T elements per tile, T/8 consumer threads): 5 = (T 2048, 4 stages, 1 CTA/SM),
+// 6 = (1024, 6, 1), 7 = (1024, 4, 2 CTAs/SM), 8 = (2048, 6, 1), 9 = (2048, 3, 2),
+// 10 = (4096, 3, 1), 11 = (4096, 2, 1), 12 = (2048, 2, 3), 13 = (1024, 4, 3)
 int adam_ctas_per_sm(int variant) {
   switch (variant) {
     case 1: return 4;
     case 3: return 3;
     case 4: return 1;
+    case 5: return 1;
+    case 6: return 1;
+    case 7: return 2;
+    case 8: return 1;
+    case 9: return 2;
+    case 10: return 1;
+    case 11: return 1;
+    case 12: return 3;
+    case 13: return 3;
     default: return 2;
   }
 }
+bool adam_variant_is_tma(int variant) { return variant >= 5 && variant <= 13; }
 
 template <int PD, int GD>
 cudaError_t launch_adam_t(const AdamArgs& a, int grid, cudaStream_t s, int variant) {
   switch (variant) {
+    case 5: return launch_adam_tma_t<PD, GD, 2048, 4>(a, grid, s);
+    case 6: return launch_adam_tma_t<PD, GD, 1024, 6>(a, grid, s);
+    case 7: return launch_adam_tma_t<PD, GD, 1024, 4>(a, grid, s);
+    case 8: return launch_adam_tma_t<PD, GD, 2048, 6>(a, grid, s);
+    case 9: return launch_adam_tma_t<PD, GD, 2048, 3>(a, grid, s);
+    case 10: return launch_adam_tma_t<PD, GD, 4096, 3>(a, grid, s);
+    case 11: return launch_adam_tma_t<PD, GD, 4096, 2>(a, grid, s);
+    case 12: return launch_adam_tma_t<PD, GD, 2048, 2>(a, grid, s);
+    case 13: return launch_adam_tma_t<PD, GD, 1024, 4>(a, grid, s);
     case 1: k_adam<PD, GD, 4, 1><<<grid, kThreads, 0, s>>>(a); break;
     case 2: k_adam<PD, GD, 2, 2><<<grid, kThreads, 0, s>>>(a); break;
     case 3: k_adam<PD, GD, 3, 1><<<grid, kThreads, 0, s>>>(a); break;

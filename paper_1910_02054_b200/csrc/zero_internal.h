@@ -65,7 +65,6 @@ struct FlatPiece {
   const void* src;          // nullptr = zero fill (alignment gap / padding)
   uint64_t dst_off;         // element offset inside the destination bucket
   uint64_t count;
-  uint64_t chunk_begin;     // prefix sum of chunks
 };
 
 struct FlatArgs {
@@ -73,7 +72,7 @@ struct FlatArgs {
   int n_pieces;
   int src_dtype, dst_dtype;
   int epilogue;             // 1: also compute the overflow flag and norm partial (N_d == 1)
-  uint64_t total_chunks;
+  uint64_t per_cta;         // contiguous destination elements per CTA (multiple of 8)
   void* dst;
   float sigma;
   const DevState* st;
@@ -136,13 +135,13 @@ struct LoadArgs {             // master init: fp32 piece -> shard / 16-bit copy
 
 // launchers (kernels.cu); return the launch error
 cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s, int vecs);
-uint32_t flat_chunk(int vecs);
 cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_decide_local(const Slot* slots, int n_slots, RankPartial* out, cudaStream_t s);
 struct PartialPtrs { const RankPartial* p[kMaxRanks]; };
 cudaError_t launch_decide_global(const PartialPtrs& partials, DevState* st, DecideParams p, cudaStream_t s);
 cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int variant);
 int adam_ctas_per_sm(int variant);
+bool adam_variant_is_tma(int variant);
 cudaError_t launch_copy(const CopyArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_load(const LoadArgs& a, cudaStream_t s);
 cudaError_t launch_init_state(DevState* st, float S, float inv, cudaStream_t s);

@@ -5,13 +5,19 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+import argparse
+ap = argparse.ArgumentParser()
+ap.add_argument("--adam", default="0,1,2,3,4")
+ap.add_argument("--flat", default="")          # e.g. "4x4,4x8"  (vecs x ctas)
+ap.add_argument("--base", default="")          # fixed env for every run, e.g. "ZERO_ADAM_VARIANT=1"
+args, extra = ap.parse_known_args()
+base = dict(kv.split("=") for kv in args.base.split(",") if kv)
 variants = []
-for av in (0, 1, 2, 3, 4):
-    variants.append({"ZERO_ADAM_VARIANT": str(av)})
-for fv in (1, 2, 4, 8):
-    for fc in (2, 4, 8):
-        variants.append({"ZERO_FLAT_VECS": str(fv), "ZERO_FLAT_CTAS": str(fc)})
-extra = sys.argv[1:]
+for av in [x for x in args.adam.split(",") if x]:
+    variants.append(dict(base, ZERO_ADAM_VARIANT=av))
+for fv in [x for x in args.flat.split(",") if x]:
+    v, c = fv.split("x")
+    variants.append(dict(base, ZERO_FLAT_VECS=v, ZERO_FLAT_CTAS=c))
 for v in variants:
     env = dict(os.environ, **v)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "30", "--no-e2e",

@@ -269,3 +269,12 @@ def gpu_grads_flat(tensors: Sequence[TensorSpec], seed: int, rank: int, step: in
         gpu_fill(v, key, o, (2.0 ** -(6 + (ti % 8))) * scale)
         views.append(v)
     return buf, views
+
+
+def uniform_at(key: int, idx: np.ndarray) -> np.ndarray:
+    """x_i at arbitrary element indices (the same stream as uniform_pm1)."""
+    idx = np.asarray(idx, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        h = _splitmix64_vec(idx + np.uint64(key))
+    q = (h >> np.uint64(40)).astype(np.int64) - (1 << 23)
+    return (q.astype(np.float32) * np.float32(2.0 ** -23)).astype(np.float32)
