@@ -186,8 +186,9 @@ struct zero_ctx {
   std::vector<AdamSeg> segs_host;
   bool segs_aligned8 = true;                       // every segment offset/count % 8 == 0
   int sms = 148;
-  int adam_variant = 0;                            // ZERO_ADAM_VARIANT (tuning experiments)
+  int adam_variant = 11;                           // ZERO_ADAM_VARIANT (tuning; 11 = TMA 4096 x 2 stages)
   int flat_vecs = 4, flat_ctas = 4;                // ZERO_FLAT_VECS / ZERO_FLAT_CTAS
+  int flat_tma = 0;                                // ZERO_FLAT_TMA: 0 off, else the TMA variant
 
   // per-step tracking
   std::vector<uint8_t> reduced;
@@ -235,7 +236,7 @@ struct zero_ctx {
   uint16_t* flat_dst(uint32_t k) const {       // where bucket k is flattened
     const zero_bucket& b = buckets[k];
     if (stage <= 1) return grad + b.base;
-    if (n_d == 1) return reinterpret_cast<uint16_t*>(gred) + b.shard_off;
+    if (transport == ZERO_TRANSPORT_LOCAL) return reinterpret_cast<uint16_t*>(gred) + b.shard_off;
     return grad + (uint64_t)(k % pool) * maxB;
   }
   // where bucket k's reduced slice (this rank's) lives
@@ -382,7 +383,7 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
   if (cfg->dynamic_loss_scale && (cfg->scale_window == 0 || !(cfg->min_loss_scale > 0.f)))
     return bad("dynamic loss scaling needs scale_window > 0 and min_loss_scale > 0");
   if (transport == ZERO_TRANSPORT_LOCAL && n_d != 1) return bad("LOCAL transport requires n_d == 1");
-  if (transport == ZERO_TRANSPORT_NCCL && n_d > 1 && !nccl_comm) return bad("NCCL transport requires a communicator");
+  if (transport == ZERO_TRANSPORT_NCCL && !nccl_comm) return bad("NCCL transport requires a communicator");
   if (transport != ZERO_TRANSPORT_LOCAL && transport != ZERO_TRANSPORT_NCCL && transport != ZERO_TRANSPORT_PEER)
     return bad("unknown transport");
   const bool r32 = cfg->reduce_mode == ZERO_R32 && n_d > 1;
@@ -399,7 +400,10 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
   c->cfg = *cfg;
   if (c->cfg.prefetch_depth == 0) c->cfg.prefetch_depth = 1;
   c->pool = c->cfg.pool_buckets ? c->cfg.pool_buckets : 2;
-  c->transport = (n_d == 1) ? ZERO_TRANSPORT_LOCAL : transport;
+  // n_d == 1 degenerates to LOCAL, except NCCL with a real (1-rank) communicator, which
+  // keeps the collective code path (used to test it on one GPU)
+  c->transport = (n_d == 1 && transport != ZERO_TRANSPORT_NCCL) ? ZERO_TRANSPORT_LOCAL : transport;
+  const bool coll = c->transport != ZERO_TRANSPORT_LOCAL;
   c->comm = reinterpret_cast<ncclComm_t>(nccl_comm);
   c->stream = reinterpret_cast<cudaStream_t>(compute_stream);
   c->pdt = to_dt(cfg->param_dtype);
@@ -491,10 +495,10 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
   z.opt_stride_elems = c->opt_stride;
   z.p16_bytes = 2ull * (stage == 3 ? S : P);
   if (stage <= 1) z.grad_bytes = 2ull * P;
-  else z.grad_bytes = (n_d > 1) ? 2ull * c->pool * c->maxB : 0;
+  else z.grad_bytes = coll ? 2ull * c->pool * c->maxB : 0;
   if (stage >= 2) z.gred_bytes = (r32 ? 4ull : 2ull) * S;
   else z.gred_bytes = r32 ? 4ull * S : 0;
-  z.gather_bytes = (stage == 3 && n_d > 1) ? 2ull * (c->cfg.prefetch_depth + 1) * c->max_layer : 0;
+  z.gather_bytes = (stage == 3 && coll) ? 2ull * (c->cfg.prefetch_depth + 1) * c->max_layer : 0;
   z.scratch_bytes = scratch_layout(c->n_slots, c->segs_host.size()).total;
 
   c->reduced.assign(c->info.n_buckets, 0);
@@ -547,6 +551,7 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   if (const char* ev = getenv("ZERO_ADAM_VARIANT")) c->adam_variant = atoi(ev);
   if (const char* ev = getenv("ZERO_FLAT_VECS")) c->flat_vecs = atoi(ev);
   if (const char* ev = getenv("ZERO_FLAT_CTAS")) c->flat_ctas = atoi(ev);
+  if (const char* ev = getenv("ZERO_FLAT_TMA")) c->flat_tma = atoi(ev);
   if (c->flat_vecs != 1 && c->flat_vecs != 2 && c->flat_vecs != 4 && c->flat_vecs != 8) c->flat_vecs = 4;
   if (c->flat_ctas < 1 || c->flat_ctas > 8) c->flat_ctas = 4;
 
@@ -643,7 +648,7 @@ zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads) {
   const auto& tmpl = c->flat_tmpl[k];
   uint16_t* dst = c->flat_dst(k);
   const int ebytes = c->gdt == DT_F32 ? 4 : 2;
-  const bool epi = c->n_d == 1;
+  const bool epi = c->transport == ZERO_TRANSPORT_LOCAL;
   int slot = c->slot_base[k];
   for (size_t b0 = 0; b0 < tmpl.size(); b0 += kMaxFlatPieces, ++slot) {
     FlatArgs a{};
@@ -662,7 +667,14 @@ zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads) {
     }
     a.n_pieces = (int)(b1 - b0);
     const uint64_t total = tmpl[b1 - 1].dst_off + tmpl[b1 - 1].count - tmpl[b0].dst_off;
-    const int grid = grid_for((total + 2047) / 2048, c->flat_ctas, c->sms);
+    // TMA staging needs 16-B granules: every piece boundary and source % 8 elements
+    bool tma_ok = c->flat_tma > 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+    for (int j = 0; tma_ok && j < (int)(b1 - b0); ++j) {
+      const FlatPiece& fp = a.pieces[j];
+      if ((fp.dst_off | fp.count) & 7) tma_ok = false;
+      if (fp.src && (reinterpret_cast<uintptr_t>(fp.src) & 15)) tma_ok = false;
+    }
+    const int grid = grid_for((total + 2047) / 2048, tma_ok ? 1 : c->flat_ctas, c->sms);
     a.per_cta = align_up((total + grid - 1) / grid, 8);
     a.src_dtype = c->gdt;
     a.dst_dtype = c->pdt;
@@ -672,7 +684,8 @@ zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads) {
     a.st = c->st;
     a.part = c->part_compute;
     a.slot = c->slots + slot;
-    CK(launch_flatten(a, grid, c->stream, c->flat_vecs));
+    if (tma_ok) CK(launch_flatten_tma(a, grid, c->stream, c->flat_tma));
+    else CK(launch_flatten(a, grid, c->stream, c->flat_vecs));
     c->launches++;
   }
   return ZERO_OK;
@@ -717,7 +730,7 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
   const void* const* grads = tensor_grads ? tensor_grads : c->grad_ptrs.data();
 
   // C_B pool slot reuse (stages 2/3, N_d > 1)
-  const bool pooled = c->stage >= 2 && c->n_d > 1;
+  const bool pooled = c->stage >= 2 && c->transport != ZERO_TRANSPORT_LOCAL;
   const uint32_t ps = pooled ? k % c->pool : 0;
   if (pooled && c->transport == ZERO_TRANSPORT_PEER) {
     const int pend = c->pool_pending[ps];
@@ -736,7 +749,7 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
   zero_status s = issue_flatten(c, k, grads);
   if (s != ZERO_OK) return s;
 
-  if (c->n_d == 1) return finish_bucket_local(c, k);
+  if (c->transport == ZERO_TRANSPORT_LOCAL) return finish_bucket_local(c, k);
 
   if (c->transport == ZERO_TRANSPORT_PEER) {
     ZeroGroup* g = c->group;
@@ -1048,7 +1061,7 @@ zero_status zero_gather_params(zero_ctx* c, uint32_t layer, void** views_out) {
   if (it == c->layer_index.end()) return c->fail(ZERO_EINVAL, "unknown layer %u", layer);
   const int li = it->second;
   uint16_t* base;
-  if (c->n_d == 1) {
+  if (c->transport == ZERO_TRANSPORT_LOCAL) {
     base = c->p16 + c->layers[li].flat0;  // the shard is the whole replica
   } else {
     if (c->last_layer >= 0) c->direction = (li >= c->last_layer) ? +1 : -1;
@@ -1089,7 +1102,7 @@ zero_status zero_release_params(zero_ctx* c, uint32_t layer) {
   if (c->stage != 3) return c->fail(ZERO_ESTATE, "zero_release_params needs stage 3");
   auto it = c->layer_index.find(layer);
   if (it == c->layer_index.end()) return c->fail(ZERO_EINVAL, "unknown layer %u", layer);
-  if (c->n_d == 1) return ZERO_OK;
+  if (c->transport == ZERO_TRANSPORT_LOCAL) return ZERO_OK;
   const int s = c->layer_slot[it->second];
   if (s < 0) return c->fail(ZERO_ESTATE, "layer %u is not gathered", layer);
   c->gslots[s].released = true;
@@ -1101,7 +1114,7 @@ zero_status zero_param_view(const zero_ctx* c, uint32_t t, void** p16) {
   if (!c || !p16) return ZERO_EINVAL;
   if (t >= c->tensors.size() || c->tensor_flat[t] == UINT64_MAX) return ZERO_EINVAL;
   if (!c->bound) return ZERO_ESTATE;
-  if (c->stage == 3 && c->n_d > 1) return ZERO_ESTATE;
+  if (c->stage == 3 && c->transport != ZERO_TRANSPORT_LOCAL) return ZERO_ESTATE;
   *p16 = c->p16 + c->tensor_flat[t];
   return ZERO_OK;
 }

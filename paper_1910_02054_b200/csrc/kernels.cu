@@ -70,6 +70,44 @@ __device__ __forceinline__ void st128(void* p, const U4& r) {
 }
 __host__ __device__ __forceinline__ bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
+// TMA (cp.async.bulk) + mbarrier helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void lds128(const void* p, uint32_t (&r)[4]) {
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(smem_u32(p)));
+}
+
 // 8 16-bit values packed in a U4
 __device__ __forceinline__ uint32_t h_get(const U4& v, int j) { return (v.x[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu; }
 __device__ __forceinline__ void h_set(U4& v, int j, uint32_t b) {
@@ -289,6 +327,182 @@ cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s, int vecs
     case 4: return launch_flatten_v<4>(a, grid, s);
     case 8: return launch_flatten_v<8>(a, grid, s);
     default: return launch_flatten_v<2>(a, grid, s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2 (TMA variant): the source pieces are streamed into shared memory by 1-D bulk
+// copies (a STAGES-deep mbarrier ring fed by one producer warp); T/8 consumer
+// threads cast/scale 8 elements each, compute the epilogue (N_d = 1) and store
+// 128-bit.  Needs every piece offset/count % 8 == 0 and 16-B aligned sources.
+// ---------------------------------------------------------------------------
+struct FlatCursor {
+  uint64_t cur, hi;
+  int p;
+  __device__ __forceinline__ bool next(const FlatArgs& a, uint32_t T, uint64_t& start, uint32_t& n, int& piece) {
+    while (cur < hi && p < a.n_pieces) {
+      const FlatPiece& pc = a.pieces[p];
+      const uint64_t pend = pc.dst_off + pc.count < hi ? pc.dst_off + pc.count : hi;
+      if (cur >= pend) { ++p; continue; }
+      start = cur;
+      const uint64_t left = pend - cur;
+      n = left < T ? (uint32_t)left : T;
+      piece = p;
+      cur += n;
+      return true;
+    }
+    return false;
+  }
+};
+
+template <int SDT, int DDT, bool kCopy, int T, int STAGES>
+__global__ void __launch_bounds__(T / 8 + 32, 1) k_flatten_tma(const __grid_constant__ FlatArgs a) {
+  using S = SrcLoad<SDT>;
+  using D = H16<DDT>;
+  constexpr int kCons = T / 8;
+  constexpr uint32_t kStageBytes = (uint32_t)T * S::kBytes;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  uint64_t* empty = full + STAGES;
+  const uint64_t r0 = a.pieces[0].dst_off;
+  const uint64_t r1 = a.pieces[a.n_pieces - 1].dst_off + a.pieces[a.n_pieces - 1].count;
+  const uint64_t lo = r0 + (uint64_t)blockIdx.x * a.per_cta;
+  const uint64_t hi = lo + a.per_cta < r1 ? lo + a.per_cta : r1;
+  int p0 = 0;
+  while (p0 + 1 < a.n_pieces && a.pieces[p0 + 1].dst_off <= lo) ++p0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kCons / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double sumsq = 0.0;
+  uint32_t flag = 0;
+  if (warp == kCons / 32) {  // ---- producer
+    if (lane == 0 && lo < hi) {
+      const uint64_t pol = policy_evict_first();
+      FlatCursor fc{lo, hi, p0};
+      uint64_t start;
+      uint32_t n;
+      int piece;
+      for (uint32_t it = 0; fc.next(a, T, start, n, piece); ++it) {
+        const int st = it % STAGES;
+        if (it >= (uint32_t)STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
+        const FlatPiece& pc = a.pieces[piece];
+        if (pc.src == nullptr) {
+          mbar_arrive(&full[st]);  // zero piece: nothing to load
+        } else {
+          mbar_expect_tx(&full[st], n * (uint32_t)S::kBytes);
+          bulk_g2s(smem + st * kStageBytes,
+                   reinterpret_cast<const char*>(pc.src) + (start - pc.dst_off) * S::kBytes, n * (uint32_t)S::kBytes,
+                   &full[st], pol);
+        }
+      }
+    }
+  } else {  // ---- consumers
+    const float sigma = a.sigma;
+    const float inv = a.epilogue ? a.st->inv_cur : 0.0f;
+    uint16_t* dst_base = reinterpret_cast<uint16_t*>(a.dst);
+    FlatCursor fc{lo, hi, p0};
+    uint64_t start;
+    uint32_t n;
+    int piece;
+    for (uint32_t it = 0; fc.next(a, T, start, n, piece); ++it) {
+      const int st = it % STAGES;
+      mbar_wait(&full[st], (it / STAGES) & 1);
+      const uint32_t e = threadIdx.x * 8;
+      if (e < n) {
+        U4 o;
+        if (a.pieces[piece].src == nullptr) {
+          o = U4{{0u, 0u, 0u, 0u}};
+        } else {
+          const unsigned char* sb = smem + st * kStageBytes + e * S::kBytes;
+          float x[8];
+          if (S::kBytes == 4) {
+            uint32_t r[4];
+            lds128(sb, r);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) x[j] = __uint_as_float(r[j]);
+            lds128(sb + 16, r);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) x[4 + j] = __uint_as_float(r[j]);
+          } else {
+            uint32_t r[4];
+            lds128(sb, r);
+            U4 g{{r[0], r[1], r[2], r[3]}};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = H16<SDT == DT_F32 ? DT_F16 : SDT>::widen(h_get(g, j));
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t b = kCopy ? D::narrow(x[j]) : D::narrow(__fmul_rn(x[j], sigma));
+            h_set(o, j, b);
+            if (a.epilogue) {
+              flag |= D::nonfinite(b);
+              const float u = __fmul_rn(D::widen(b), inv);
+              sumsq += (double)u * (double)u;
+            }
+          }
+        }
+        st128(dst_base + start + e, o);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+  }
+  if (a.epilogue) {
+    __syncthreads();
+    grid_publish(sumsq, flag, a.part, a.slot);
+  }
+}
+
+template <int SD, int DD, bool CP, int T, int STAGES>
+cudaError_t launch_flatten_tma_t(const FlatArgs& a, int grid, cudaStream_t s) {
+  const size_t smem = (size_t)STAGES * T * SrcLoad<SD>::kBytes + 2 * STAGES * sizeof(uint64_t);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_flatten_tma<SD, DD, CP, T, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k_flatten_tma<SD, DD, CP, T, STAGES><<<grid, T / 8 + 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+// TMA flatten variants (T, STAGES): 1 = (4096, 4), 2 = (8192, 4), 3 = (4096, 8), 4 = (2048, 8)
+template <int T, int STAGES>
+cudaError_t launch_flatten_tma_ts(const FlatArgs& a, int grid, cudaStream_t s) {
+  const bool copy = (a.sigma == 1.0f) && (a.src_dtype == a.dst_dtype);
+#define ZT(SD, DD, CP) return launch_flatten_tma_t<SD, DD, CP, T, STAGES>(a, grid, s)
+  if (a.dst_dtype == DT_F16) {
+    if (a.src_dtype == DT_F16) { if (copy) ZT(DT_F16, DT_F16, true); else ZT(DT_F16, DT_F16, false); }
+    if (a.src_dtype == DT_F32) ZT(DT_F32, DT_F16, false);
+  } else if (a.dst_dtype == DT_BF16) {
+    if (a.src_dtype == DT_BF16) { if (copy) ZT(DT_BF16, DT_BF16, true); else ZT(DT_BF16, DT_BF16, false); }
+    if (a.src_dtype == DT_F32) ZT(DT_F32, DT_BF16, false);
+  }
+#undef ZT
+  return cudaErrorInvalidValue;
+}
+
+int flatten_tma_threads(int variant) {
+  switch (variant) {
+    case 2: return 8192 / 8 + 32;
+    case 4: return 2048 / 8 + 32;
+    default: return 4096 / 8 + 32;
+  }
+}
+
+cudaError_t launch_flatten_tma(const FlatArgs& a, int grid, cudaStream_t s, int variant) {
+  switch (variant) {
+    case 2: return launch_flatten_tma_ts<8192, 4>(a, grid, s);
+    case 3: return launch_flatten_tma_ts<4096, 8>(a, grid, s);
+    case 4: return launch_flatten_tma_ts<2048, 8>(a, grid, s);
+    default: return launch_flatten_tma_ts<4096, 4>(a, grid, s);
   }
 }
 
@@ -632,43 +846,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_adam(const __grid_constant__
 // compute from shared memory and store p32/m/v/p16 with 256/128-bit STG.
 // Requires every segment offset and count to be a multiple of 8 (host checks).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void lds128(const void* p, uint32_t (&r)[4]) {
-  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(smem_u32(p)));
-}
-
 // tile iterator over the CTA's contiguous range, split at segment boundaries
 struct TileCursor {
   uint64_t cur, hi;
@@ -835,7 +1012,8 @@ cudaError_t launch_adam_tma_t(const AdamArgs& a, int grid, cudaStream_t s) {
 // variants: 0 = (2 CTAs/SM, U=1), 1 = (4, 1), 2 = (2, 2), 3 = (3, 1), 4 = (1, 4),
 // TMA (T elements per tile, T/8 consumer threads): 5 = (T 2048, 4 stages, 1 CTA/SM),
 // 6 = (1024, 6, 1), 7 = (1024, 4, 2 CTAs/SM), 8 = (2048, 6, 1), 9 = (2048, 3, 2),
-// 10 = (4096, 3, 1), 11 = (4096, 2, 1), 12 = (2048, 2, 3), 13 = (1024, 4, 3)
+// 10 = (4096, 3, 1), 11 = (4096, 2, 1), 12 = (2048, 2, 3), 13 = (1024, 4, 3),
+// 14 = (6144, 2, 1), 15 = (3072, 2, 2), 16 = (2048, 2, 2), 17 = (4096, 1, 2), 18 = (2048, 4, 2)
 int adam_ctas_per_sm(int variant) {
   switch (variant) {
     case 1: return 4;
@@ -850,10 +1028,15 @@ int adam_ctas_per_sm(int variant) {
     case 11: return 1;
     case 12: return 3;
     case 13: return 3;
+    case 14: return 1;
+    case 15: return 2;
+    case 16: return 2;
+    case 17: return 2;
+    case 18: return 2;
     default: return 2;
   }
 }
-bool adam_variant_is_tma(int variant) { return variant >= 5 && variant <= 13; }
+bool adam_variant_is_tma(int variant) { return variant >= 5 && variant <= 18; }
 
 template <int PD, int GD>
 cudaError_t launch_adam_t(const AdamArgs& a, int grid, cudaStream_t s, int variant) {
@@ -867,6 +1050,11 @@ cudaError_t launch_adam_t(const AdamArgs& a, int grid, cudaStream_t s, int varia
     case 11: return launch_adam_tma_t<PD, GD, 4096, 2>(a, grid, s);
     case 12: return launch_adam_tma_t<PD, GD, 2048, 2>(a, grid, s);
     case 13: return launch_adam_tma_t<PD, GD, 1024, 4>(a, grid, s);
+    case 14: return launch_adam_tma_t<PD, GD, 6144, 2>(a, grid, s);
+    case 15: return launch_adam_tma_t<PD, GD, 3072, 2>(a, grid, s);
+    case 16: return launch_adam_tma_t<PD, GD, 2048, 2>(a, grid, s);
+    case 17: return launch_adam_tma_t<PD, GD, 4096, 1>(a, grid, s);
+    case 18: return launch_adam_tma_t<PD, GD, 2048, 4>(a, grid, s);
     case 1: k_adam<PD, GD, 4, 1><<<grid, kThreads, 0, s>>>(a); break;
     case 2: k_adam<PD, GD, 2, 2><<<grid, kThreads, 0, s>>>(a); break;
     case 3: k_adam<PD, GD, 3, 1><<<grid, kThreads, 0, s>>>(a); break;

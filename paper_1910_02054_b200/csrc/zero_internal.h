@@ -135,6 +135,7 @@ struct LoadArgs {             // master init: fp32 piece -> shard / 16-bit copy
 
 // launchers (kernels.cu); return the launch error
 cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s, int vecs);
+cudaError_t launch_flatten_tma(const FlatArgs& a, int grid, cudaStream_t s, int variant);
 cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_decide_local(const Slot* slots, int n_slots, RankPartial* out, cudaStream_t s);
 struct PartialPtrs { const RankPartial* p[kMaxRanks]; };

@@ -43,7 +43,8 @@ class Run:
     cap: int = 1 << 17
     seed: int = 1
     inject: Sequence[int] = ()          # steps (0-based) with +inf at rank min(1,n-1), flat index Psi//2
-    grad_scale_fn = None
+    transport: str = "local"            # n == 1: "local" or "nccl" (1-rank communicator)
+    nccl_comm: int = 0
 
 
 class Pair:
@@ -58,8 +59,8 @@ class Pair:
         self.lay = OL.make_layout(self.numels, self.layers, run.n, run.align, run.cap)
         zc = zcfg_from_oracle(run.cfg)
         if run.n == 1:
-            self.engines = [ZeroEngine(self.numels, self.layers, 1, 0, run.stage, zc, "local",
-                                       align=run.align, bucket_cap=run.cap)]
+            self.engines = [ZeroEngine(self.numels, self.layers, 1, 0, run.stage, zc, run.transport,
+                                       nccl_comm=run.nccl_comm, align=run.align, bucket_cap=run.cap)]
             self.group = None
         else:
             self.group = ZeroSimGroup(self.numels, self.layers, run.n, run.stage, zc, run.align, run.cap)
