@@ -215,6 +215,20 @@ zero_status zero_bind_buffers(struct zero_ctx* ctx, const zero_buffers* bufs);
  * may run once every rank reduced every bucket of the step. */
 zero_status zero_sim_group(struct zero_ctx* const* ranks, int n);
 
+/* PEER across processes (one process per GPU, or several on one GPU): export this
+ * rank's peer-visible arenas (grad, p16, scratch) as an opaque blob of CUDA IPC
+ * handles + offsets; exchange the blobs (e.g. torch.distributed.all_gather_object)
+ * and install all n_d of them, in rank order, with zero_peer_open.  Afterwards the
+ * pull reduce-scatter reads peers' buckets over NVLink, the Adam kernel stores the
+ * recast parameters into every peer's replica (fused all-gather), and device-side
+ * release/acquire signals at system scope order the ranks (no host barrier).
+ * zero_peer_export with blob == NULL returns the blob size in *blob_bytes.
+ * Errors: ZERO_ESTATE (not an unlinked, bound PEER context), ZERO_EINVAL (a blob of
+ * another rank/layout/stage), ZERO_ECUDA (IPC failure; the arenas must come from
+ * cudaMalloc-backed memory without expandable segments). */
+zero_status zero_peer_export(struct zero_ctx* ctx, void* blob, size_t* blob_bytes);
+zero_status zero_peer_open(struct zero_ctx* ctx, const void* const* blobs, size_t blob_bytes);
+
 /* Initialise the model states from the full fp32 master weights: tensor_master[t]
  * is a device pointer to tensor t's numel fp32 values (every rank passes the same
  * values).  Writes this rank's fp32 shard, zeroes m and v, t = 0, and writes the

@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <dlfcn.h>
 #include <cstring>
 #include <map>
 #include <string>
@@ -209,6 +210,19 @@ struct zero_ctx {
   ZeroGroup* group = nullptr;
   zero_comm_counters counters{};
 
+  // cross-process PEER (CUDA IPC) peer table
+  bool ipc = false;
+  uint16_t* peer_grad[ZERO_MAX_RANKS] = {};
+  uint16_t* peer_p16[ZERO_MAX_RANKS] = {};
+  char* peer_scratch[ZERO_MAX_RANKS] = {};
+  std::vector<void*> ipc_mapped;                   // bases to cudaIpcCloseMemHandle
+  std::vector<std::pair<int, uint64_t>> pool_last; // per pool slot: (bucket, epoch) of its last use
+  size_t off_sig_flat = 0, off_sig_rs = 0, off_sig_part = 0, off_sig_adam = 0, off_gathered = 0;
+  uint64_t epoch() const { return counters.steps + 1; }
+  uint64_t* sig(int r, size_t off, size_t idx) const {  // signal slot in rank r's scratch
+    return reinterpret_cast<uint64_t*>(peer_scratch[r] + off) + idx;
+  }
+
   // phase timing (cfg.timing): one event set per step, reused from a pool
   struct StepEvents { cudaEvent_t r0 = nullptr, r1 = nullptr, a0 = nullptr, a1 = nullptr, s1 = nullptr; };
   std::vector<StepEvents> ev_pool;
@@ -304,9 +318,11 @@ int grid_for(uint64_t work_items, int per_sm, int sms) {
 
 // bytes of the scratch arena and the offsets inside it
 struct ScratchLayout {
-  size_t st, slots, part_compute, part_comm, my_partial, gathered, segs, total;
+  size_t st, slots, part_compute, part_comm, my_partial, gathered, segs, sig_flat, sig_rs, sig_part, sig_adam, total;
 };
-ScratchLayout scratch_layout(int n_slots, size_t n_segs) {
+// sig_flat[k][r] / sig_rs[k][r]: epoch at which rank r flattened / finished reducing bucket k
+// sig_part[r] / sig_adam[r]: epoch at which rank r published its partial / finished Adam
+ScratchLayout scratch_layout(int n_slots, size_t n_segs, size_t n_buckets) {
   ScratchLayout s{};
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
@@ -317,6 +333,10 @@ ScratchLayout scratch_layout(int n_slots, size_t n_segs) {
   s.my_partial = take(sizeof(RankPartial));
   s.gathered = take(sizeof(RankPartial) * ZERO_MAX_RANKS);
   s.segs = take(sizeof(AdamSeg) * std::max<size_t>(n_segs, 1));
+  s.sig_flat = take(sizeof(uint64_t) * ZERO_MAX_RANKS * std::max<size_t>(n_buckets, 1));
+  s.sig_rs = take(sizeof(uint64_t) * ZERO_MAX_RANKS * std::max<size_t>(n_buckets, 1));
+  s.sig_part = take(sizeof(uint64_t) * ZERO_MAX_RANKS);
+  s.sig_adam = take(sizeof(uint64_t) * ZERO_MAX_RANKS);
   s.total = o;
   return s;
 }
@@ -499,7 +519,7 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
   if (stage >= 2) z.gred_bytes = (r32 ? 4ull : 2ull) * S;
   else z.gred_bytes = r32 ? 4ull * S : 0;
   z.gather_bytes = (stage == 3 && coll) ? 2ull * (c->cfg.prefetch_depth + 1) * c->max_layer : 0;
-  z.scratch_bytes = scratch_layout(c->n_slots, c->segs_host.size()).total;
+  z.scratch_bytes = scratch_layout(c->n_slots, c->segs_host.size(), c->buckets.size()).total;
 
   c->reduced.assign(c->info.n_buckets, 0);
   c->pool_pending.assign(c->pool, -1);
@@ -538,7 +558,7 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   c->grad = reinterpret_cast<uint16_t*>(b->grad);
   c->gred = b->gred;
   c->gather = reinterpret_cast<uint16_t*>(b->gather);
-  const ScratchLayout sl = scratch_layout(c->n_slots, c->segs_host.size());
+  const ScratchLayout sl = scratch_layout(c->n_slots, c->segs_host.size(), c->buckets.size());
   char* s = reinterpret_cast<char*>(b->scratch);
   c->st = reinterpret_cast<DevState*>(s + sl.st);
   c->slots = reinterpret_cast<Slot*>(s + sl.slots);
@@ -547,6 +567,12 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   c->my_partial = reinterpret_cast<RankPartial*>(s + sl.my_partial);
   c->gathered = reinterpret_cast<RankPartial*>(s + sl.gathered);
   c->segs = reinterpret_cast<AdamSeg*>(s + sl.segs);
+  c->off_sig_flat = sl.sig_flat;
+  c->off_sig_rs = sl.sig_rs;
+  c->off_sig_part = sl.sig_part;
+  c->off_sig_adam = sl.sig_adam;
+  c->off_gathered = sl.gathered;
+  c->pool_last.assign(c->pool, std::make_pair(-1, (uint64_t)0));
   c->sms = sm_count();
   if (const char* ev = getenv("ZERO_ADAM_VARIANT")) c->adam_variant = atoi(ev);
   if (const char* ev = getenv("ZERO_FLAT_VECS")) c->flat_vecs = atoi(ev);
@@ -726,13 +752,22 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
   if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
   if (k >= c->info.n_buckets) return c->fail(ZERO_EINVAL, "bucket %u out of range", k);
   if (c->reduced[k]) return c->fail(ZERO_ESTATE, "bucket %u already reduced this step", k);
-  if (c->transport == ZERO_TRANSPORT_PEER && !c->group) return c->fail(ZERO_ESTATE, "PEER context not in a group");
+  if (c->transport == ZERO_TRANSPORT_PEER && !c->group && !c->ipc)
+    return c->fail(ZERO_ESTATE, "PEER context neither in a group nor linked by zero_peer_open");
   const void* const* grads = tensor_grads ? tensor_grads : c->grad_ptrs.data();
 
   // C_B pool slot reuse (stages 2/3, N_d > 1)
   const bool pooled = c->stage >= 2 && c->transport != ZERO_TRANSPORT_LOCAL;
   const uint32_t ps = pooled ? k % c->pool : 0;
-  if (pooled && c->transport == ZERO_TRANSPORT_PEER) {
+  if (pooled && c->ipc) {  // every peer finished reading this slot's previous bucket
+    const auto& pl = c->pool_last[ps];
+    if (pl.first >= 0) {
+      WaitArgs w{c->sig(c->rank, c->off_sig_rs, (size_t)pl.first * ZERO_MAX_RANKS), c->n_d, pl.second};
+      CK(launch_wait(w, c->stream));
+      c->launches++;
+    }
+  }
+  if (pooled && c->transport == ZERO_TRANSPORT_PEER && c->group) {
     const int pend = c->pool_pending[ps];
     if (pend >= 0 && c->group->flat_count[pend] < c->group->n)
       return c->fail(ZERO_ESTATE, "pool slot %u still holds bucket %d awaiting its reduce-scatter", ps, pend);
@@ -750,6 +785,56 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
   if (s != ZERO_OK) return s;
 
   if (c->transport == ZERO_TRANSPORT_LOCAL) return finish_bucket_local(c, k);
+
+  if (c->ipc) {  // cross-process PEER: signal "flattened", pull-reduce my slice, signal "read done"
+    const uint64_t ep = c->epoch();
+    const size_t kk = (size_t)k * ZERO_MAX_RANKS;
+    SigArgs sa{};
+    for (int j = 0; j < c->n_d; ++j) sa.dst[j] = c->sig(j, c->off_sig_flat, kk + c->rank);
+    sa.n = c->n_d;
+    sa.epoch = ep;
+    CK(launch_signal(sa, c->stream));
+    c->launches++;
+    const uint64_t sl = c->slice(k);
+    const size_t foff = (size_t)(c->flat_dst(k) - c->grad);
+    RSArgs a{};
+    for (int j = 0; j < c->n_d; ++j) {
+      a.src[j] = c->peer_grad[j] + foff + (uint64_t)c->rank * sl;
+      a.done_sig[j] = c->sig(j, c->off_sig_rs, kk + c->rank);
+    }
+    a.wait_flags = c->sig(c->rank, c->off_sig_flat, kk);
+    a.epoch = ep;
+    a.dst = c->rs_dst(k);
+    a.count = sl;
+    a.n = c->n_d;
+    a.dtype = c->pdt;
+    a.r32 = c->r32 ? 1 : 0;
+    a.reduce = 1;
+    a.st = c->st;
+    a.part = c->part_comm;
+    a.slot = c->slots + c->slot_base[k];
+    CK(launch_reduce_scatter(a, grid_for((sl + 2047) / 2048, 4, c->sms), c->stream));
+    c->launches++;
+    c->counters.reduce_scatter += sl * (uint64_t)(c->n_d - 1);
+    if (c->stage == 0) {  // all-reduce = RS + AG of the reduced slices
+      WaitArgs w{c->sig(c->rank, c->off_sig_rs, kk), c->n_d, ep};
+      CK(launch_wait(w, c->stream));
+      c->launches++;
+      CopyArgs ca{};
+      const zero_bucket& b = c->buckets[k];
+      for (int i = 0; i < c->n_d; ++i) {
+        ca.src[i] = c->peer_grad[i] + b.base + (uint64_t)i * sl;
+        ca.dst[i] = c->grad + b.base + (uint64_t)i * sl;
+      }
+      ca.count = sl;
+      ca.n = c->n_d;
+      CK(launch_copy(ca, grid_for((sl + 2047) / 2048, 2, c->sms), c->stream));
+      c->launches++;
+      c->counters.all_gather += sl * (uint64_t)(c->n_d - 1);
+    }
+    if (pooled) c->pool_last[ps] = std::make_pair((int)k, ep);
+    return finish_bucket_local(c, k);
+  }
 
   if (c->transport == ZERO_TRANSPORT_PEER) {
     ZeroGroup* g = c->group;
@@ -836,6 +921,9 @@ zero_status issue_adam(zero_ctx* c, ZeroGroup* g) {
   if (g && (c->stage == 1 || c->stage == 2)) {  // fused all-gather: store into every replica
     a.n_p16 = g->n;
     for (int j = 0; j < g->n; ++j) a.p16[j] = g->ranks[j]->p16;
+  } else if (c->ipc && (c->stage == 1 || c->stage == 2)) {  // same, through the IPC peer table
+    a.n_p16 = c->n_d;
+    for (int j = 0; j < c->n_d; ++j) a.p16[j] = c->peer_p16[j];
   } else {
     a.n_p16 = 1;
     a.p16[0] = c->p16;
@@ -909,6 +997,22 @@ zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
     CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream));
     c->launches++;
     pp.p[0] = c->my_partial;
+  } else if (c->ipc) {  // push my partial into every peer's gathered[rank], then wait for all
+    CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream));
+    c->launches++;
+    PushArgs pa{};
+    pa.mine = c->my_partial;
+    for (int j = 0; j < c->n_d; ++j) {
+      pa.dst[j] = reinterpret_cast<RankPartial*>(c->peer_scratch[j] + c->off_gathered) + c->rank;
+      pa.sig[j] = c->sig(j, c->off_sig_part, c->rank);
+    }
+    pa.n = c->n_d;
+    pa.epoch = c->epoch();
+    CK(launch_push_partial(pa, c->comm_stream));
+    c->launches++;
+    for (int j = 0; j < c->n_d; ++j) pp.p[j] = c->gathered + j;
+    pp.wait_flags = c->sig(c->rank, c->off_sig_part, 0);
+    pp.epoch = c->epoch();
   } else if (c->transport == ZERO_TRANSPORT_PEER) {
     for (int j = 0; j < g->n; ++j) pp.p[j] = g->ranks[j]->my_partial;
   } else {
@@ -938,6 +1042,16 @@ zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
   } else if (c->transport == ZERO_TRANSPORT_PEER && (c->stage == 1 || c->stage == 2)) {
     for (uint32_t k = 0; k < c->info.n_buckets; ++k) c->counters.all_gather += c->slice(k) * (uint64_t)(c->n_d - 1);
   }
+  if (c->ipc) {  // the replicas (stages 1/2) / shards (stage 3) are final on every rank
+    SigArgs sa{};
+    for (int j = 0; j < c->n_d; ++j) sa.dst[j] = c->sig(j, c->off_sig_adam, c->rank);
+    sa.n = c->n_d;
+    sa.epoch = c->epoch();
+    CK(launch_signal(sa, c->comm_stream));
+    WaitArgs w{c->sig(c->rank, c->off_sig_adam, 0), c->n_d, c->epoch()};
+    CK(launch_wait(w, c->comm_stream));
+    c->launches += 2;
+  }
   if (host_out)
     CK(cudaMemcpyAsync(host_out, &c->st->rec_t, sizeof(zero_step_info), cudaMemcpyDeviceToHost, c->comm_stream));
   if (ev) {
@@ -964,6 +1078,115 @@ zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
   } else {
     reset_step(c);
   }
+  return ZERO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// cross-process PEER transport over CUDA IPC
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+namespace {
+
+struct IpcRegion {
+  cudaIpcMemHandle_t handle;
+  uint64_t offset;   // of the arena inside its cudaMalloc allocation
+  uint64_t bytes;
+};
+struct IpcBlob {
+  uint32_t magic, rank, n_d, stage;
+  uint64_t psi_padded, scratch_bytes;
+  IpcRegion region[3];  // grad, p16, scratch
+};
+constexpr uint32_t kIpcMagic = 0x5A45524Fu;  // "ZERO"
+
+typedef int (*cuMemGetAddressRange_t)(unsigned long long*, size_t*, unsigned long long);
+cuMemGetAddressRange_t get_range_fn() {
+  static cuMemGetAddressRange_t fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libcuda.so.1", RTLD_NOW);
+    if (h) fn = reinterpret_cast<cuMemGetAddressRange_t>(dlsym(h, "cuMemGetAddressRange_v2"));
+  }
+  return fn;
+}
+
+}  // namespace
+
+extern "C" {
+
+zero_status zero_peer_export(zero_ctx* c, void* blob, size_t* blob_bytes) {
+  STICKY(c);
+  if (!blob_bytes) return c->fail(ZERO_EINVAL, "blob_bytes is NULL");
+  if (!blob) { *blob_bytes = sizeof(IpcBlob); return ZERO_OK; }
+  if (*blob_bytes < sizeof(IpcBlob)) return c->fail(ZERO_EINVAL, "blob buffer too small (%zu)", sizeof(IpcBlob));
+  if (c->transport != ZERO_TRANSPORT_PEER || c->group) return c->fail(ZERO_ESTATE, "export needs an ungrouped PEER context");
+  if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
+  auto range = get_range_fn();
+  if (!range) return c->fail(ZERO_ECUDA, "cuMemGetAddressRange unavailable");
+  IpcBlob b{};
+  b.magic = kIpcMagic;
+  b.rank = (uint32_t)c->rank;
+  b.n_d = (uint32_t)c->n_d;
+  b.stage = (uint32_t)c->stage;
+  b.psi_padded = c->info.psi_padded;
+  b.scratch_bytes = c->sizes.scratch_bytes;
+  const void* ptrs[3] = {c->bufs.grad, c->bufs.p16, c->bufs.scratch};
+  const uint64_t sz[3] = {c->sizes.grad_bytes, c->sizes.p16_bytes, c->sizes.scratch_bytes};
+  for (int i = 0; i < 3; ++i) {
+    if (!sz[i]) continue;
+    unsigned long long base = 0;
+    size_t bsz = 0;
+    if (range(&base, &bsz, (unsigned long long)reinterpret_cast<uintptr_t>(ptrs[i])) != 0)
+      return c->fail(ZERO_ECUDA, "cuMemGetAddressRange failed for arena %d", i);
+    CK(cudaIpcGetMemHandle(&b.region[i].handle, reinterpret_cast<void*>(base)));
+    b.region[i].offset = reinterpret_cast<uintptr_t>(ptrs[i]) - base;
+    b.region[i].bytes = sz[i];
+  }
+  std::memcpy(blob, &b, sizeof(b));
+  *blob_bytes = sizeof(b);
+  return ZERO_OK;
+}
+
+zero_status zero_peer_open(zero_ctx* c, const void* const* blobs, size_t blob_bytes) {
+  STICKY(c);
+  if (!blobs || blob_bytes < sizeof(IpcBlob)) return c->fail(ZERO_EINVAL, "bad blobs");
+  if (c->transport != ZERO_TRANSPORT_PEER || c->group || c->ipc) return c->fail(ZERO_ESTATE, "open needs an unlinked PEER context");
+  if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
+  for (int r = 0; r < c->n_d; ++r) {
+    IpcBlob b;
+    std::memcpy(&b, blobs[r], sizeof(b));
+    if (b.magic != kIpcMagic || (int)b.rank != r || (int)b.n_d != c->n_d || (int)b.stage != c->stage ||
+        b.psi_padded != c->info.psi_padded || b.scratch_bytes != c->sizes.scratch_bytes)
+      return c->fail(ZERO_EINVAL, "blob %d does not match this context (rank/layout/stage)", r);
+    if (r == c->rank) {
+      c->peer_grad[r] = c->grad;
+      c->peer_p16[r] = c->p16;
+      c->peer_scratch[r] = reinterpret_cast<char*>(c->bufs.scratch);
+      continue;
+    }
+    void* mapped[3] = {nullptr, nullptr, nullptr};
+    void* bases[3] = {nullptr, nullptr, nullptr};
+    for (int i = 0; i < 3; ++i) {
+      if (!b.region[i].bytes) continue;
+      void* base = nullptr;
+      for (int j = 0; j < i; ++j)  // arenas of one cudaMalloc segment share a handle: map it once
+        if (bases[j] && !std::memcmp(&b.region[j].handle, &b.region[i].handle, sizeof(cudaIpcMemHandle_t)))
+          base = bases[j];
+      if (!base) {
+        CK(cudaIpcOpenMemHandle(&base, b.region[i].handle, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_mapped.push_back(base);
+      }
+      bases[i] = base;
+      mapped[i] = reinterpret_cast<char*>(base) + b.region[i].offset;
+    }
+    c->peer_grad[r] = reinterpret_cast<uint16_t*>(mapped[0]);
+    c->peer_p16[r] = reinterpret_cast<uint16_t*>(mapped[1]);
+    c->peer_scratch[r] = reinterpret_cast<char*>(mapped[2]);
+  }
+  c->ipc = true;
   return ZERO_OK;
 }
 
@@ -1015,12 +1238,12 @@ zero_status issue_layer_gather(zero_ctx* c, int li, int slot) {
       const zero_bucket& b = c->buckets[k];
       const uint64_t sl = c->slice(k);
       CopyArgs a{};
-      for (int j = 0; j < g->n; ++j) {
-        a.src[j] = g->ranks[j]->p16 + b.shard_off;
+      for (int j = 0; j < c->n_d; ++j) {
+        a.src[j] = (g ? g->ranks[j]->p16 : c->peer_p16[j]) + b.shard_off;
         a.dst[j] = dst + (b.base - L.flat0) + (uint64_t)j * sl;
       }
       a.count = sl;
-      a.n = g->n;
+      a.n = c->n_d;
       CK(launch_copy(a, grid_for((sl + 2047) / 2048, 2, c->sms), c->stream));
       c->launches++;
       c->counters.all_gather += sl * (uint64_t)(c->n_d - 1);
@@ -1231,6 +1454,7 @@ void zero_destroy(zero_ctx* c) {
       if (g->ranks[j]) g->ranks[j]->group = nullptr;
     delete g;
   }
+  for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
   for (auto& e : c->ev_pool_free) if (e) cudaEventDestroy(e);
   for (auto& e : c->ev_pool) {
     cudaEventDestroy(e.r0);

@@ -70,6 +70,20 @@ __device__ __forceinline__ void st128(void* p, const U4& r) {
 }
 __host__ __device__ __forceinline__ bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
+// cross-process signalling (system scope)
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_all(const uint64_t* flags, int n, uint64_t epoch) {
+  for (int j = 0; j < n; ++j)
+    while (ld_acquire_sys(flags + j) < epoch) __nanosleep(100);
+}
+
 // TMA (cp.async.bulk) + mbarrier helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -143,7 +157,8 @@ __device__ __forceinline__ void block_reduce(double& s, uint32_t& f) {
   }
 }
 
-__device__ void grid_publish(double s, uint32_t f, GridPartials* part, Slot* slot) {
+__device__ void grid_publish(double s, uint32_t f, GridPartials* part, Slot* slot, uint64_t* const* done_sig = nullptr,
+                             int n_done = 0, uint64_t epoch = 0) {
   __shared__ bool is_last;
   block_reduce(s, f);
   if (threadIdx.x == 0) {
@@ -167,6 +182,10 @@ __device__ void grid_publish(double s, uint32_t f, GridPartials* part, Slot* slo
     slot->sumsq = a;
     slot->flag = b;
     part->ticket = 0;
+    if (n_done) {  // every CTA has consumed its peer data: tell the peers
+      __threadfence_system();
+      for (int j = 0; j < n_done; ++j) st_release_sys(done_sig[j], epoch);
+    }
   }
 }
 
@@ -473,7 +492,8 @@ cudaError_t launch_flatten_tma_t(const FlatArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// TMA flatten variants (T, STAGES): 1 = (4096, 4), 2 = (8192, 4), 3 = (4096, 8), 4 = (2048, 8)
+// TMA flatten variants (T, STAGES): 1 = (4096, 4), 3 = (4096, 8), 4 = (2048, 8)
+// (measured slower than the register-staged k_flatten on B200: off by default)
 template <int T, int STAGES>
 cudaError_t launch_flatten_tma_ts(const FlatArgs& a, int grid, cudaStream_t s) {
   const bool copy = (a.sigma == 1.0f) && (a.src_dtype == a.dst_dtype);
@@ -489,17 +509,8 @@ cudaError_t launch_flatten_tma_ts(const FlatArgs& a, int grid, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
-int flatten_tma_threads(int variant) {
-  switch (variant) {
-    case 2: return 8192 / 8 + 32;
-    case 4: return 2048 / 8 + 32;
-    default: return 4096 / 8 + 32;
-  }
-}
-
 cudaError_t launch_flatten_tma(const FlatArgs& a, int grid, cudaStream_t s, int variant) {
   switch (variant) {
-    case 2: return launch_flatten_tma_ts<8192, 4>(a, grid, s);
     case 3: return launch_flatten_tma_ts<4096, 8>(a, grid, s);
     case 4: return launch_flatten_tma_ts<2048, 8>(a, grid, s);
     default: return launch_flatten_tma_ts<4096, 4>(a, grid, s);
@@ -514,6 +525,10 @@ cudaError_t launch_flatten_tma(const FlatArgs& a, int grid, cudaStream_t s, int 
 template <int DT, bool kR32, bool kReduce, bool kVec>
 __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_constant__ RSArgs a) {
   using D = H16<DT>;
+  if (a.wait_flags) {  // every rank has flattened this bucket (cross-process PEER)
+    if (threadIdx.x == 0) wait_all(a.wait_flags, a.n, a.epoch);
+    __syncthreads();
+  }
   const float inv = a.st->inv_cur;
   double sumsq = 0.0;
   uint32_t flag = 0;
@@ -593,7 +608,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
       }
     }
   }
-  grid_publish(sumsq, flag, a.part, a.slot);
+  grid_publish(sumsq, flag, a.part, a.slot, a.done_sig, a.wait_flags ? a.n : 0, a.epoch);
 }
 
 cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s) {
@@ -638,6 +653,7 @@ cudaError_t launch_decide_local(const Slot* slots, int n_slots, RankPartial* out
 
 __global__ void k_decide_global(const __grid_constant__ PartialPtrs pp, DevState* st, const DecideParams p) {
   if (threadIdx.x != 0) return;
+  if (pp.wait_flags) wait_all(pp.wait_flags, p.n_ranks, pp.epoch);
   double sum = 0.0, flags = 0.0;
   for (int r = 0; r < p.n_ranks; ++r) {
     sum += pp.p[r]->sumsq;
@@ -1127,6 +1143,37 @@ cudaError_t launch_load(const LoadArgs& a, cudaStream_t s) {
   const int grid = (int)(blocks < 4096 ? blocks : 4096);
   if (a.p_dtype == DT_F16) k_load<DT_F16><<<grid, kThreads, 0, s>>>(a);
   else k_load<DT_BF16><<<grid, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// cross-process PEER signalling
+// ---------------------------------------------------------------------------
+__global__ void k_signal(const __grid_constant__ SigArgs a) {
+  if (threadIdx.x == 0) __threadfence_system();
+  __syncwarp();
+  if ((int)threadIdx.x < a.n) st_release_sys(a.dst[threadIdx.x], a.epoch);
+}
+__global__ void k_wait(const __grid_constant__ WaitArgs a) {
+  if (threadIdx.x == 0) wait_all(a.flags, a.n, a.epoch);
+}
+__global__ void k_push_partial(const __grid_constant__ PushArgs a) {
+  const int j = threadIdx.x;
+  if (j < a.n) {
+    *a.dst[j] = *a.mine;
+    st_release_sys(a.sig[j], a.epoch);
+  }
+}
+cudaError_t launch_signal(const SigArgs& a, cudaStream_t s) {
+  k_signal<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_wait(const WaitArgs& a, cudaStream_t s) {
+  k_wait<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_push_partial(const PushArgs& a, cudaStream_t s) {
+  k_push_partial<<<1, 32, 0, s>>>(a);
   return cudaGetLastError();
 }
 

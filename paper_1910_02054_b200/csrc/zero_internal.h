@@ -82,6 +82,11 @@ struct FlatArgs {
 
 struct RSArgs {
   const void* src[kMaxRanks];   // rank j's bucket slice (16-bit)
+  // cross-process PEER: wait until wait_flags[0..n) >= epoch before reading peers,
+  // and store epoch into done_sig[0..n) (peers' "reduce-scatter done" slots) at the end
+  const uint64_t* wait_flags;
+  uint64_t* done_sig[kMaxRanks];
+  uint64_t epoch;
   void* dst;                    // reduced slice: 16-bit (R16) or fp32 (R32)
   uint64_t count;
   int n;
@@ -138,7 +143,32 @@ cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s, int vecs
 cudaError_t launch_flatten_tma(const FlatArgs& a, int grid, cudaStream_t s, int variant);
 cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_decide_local(const Slot* slots, int n_slots, RankPartial* out, cudaStream_t s);
-struct PartialPtrs { const RankPartial* p[kMaxRanks]; };
+struct PartialPtrs {
+  const RankPartial* p[kMaxRanks];
+  const uint64_t* wait_flags;   // cross-process PEER: wait until wait_flags[r] >= epoch
+  uint64_t epoch;
+};
+
+struct SigArgs {                // store epoch into n (peer) signal slots, release at system scope
+  uint64_t* dst[kMaxRanks];
+  int n;
+  uint64_t epoch;
+};
+struct WaitArgs {               // spin until flags[0..n) >= epoch (acquire at system scope)
+  const uint64_t* flags;
+  int n;
+  uint64_t epoch;
+};
+struct PushArgs {               // copy my partial into every peer's gathered[me], then signal
+  const RankPartial* mine;
+  RankPartial* dst[kMaxRanks];
+  uint64_t* sig[kMaxRanks];
+  int n;
+  uint64_t epoch;
+};
+cudaError_t launch_signal(const SigArgs& a, cudaStream_t s);
+cudaError_t launch_wait(const WaitArgs& a, cudaStream_t s);
+cudaError_t launch_push_partial(const PushArgs& a, cudaStream_t s);
 cudaError_t launch_decide_global(const PartialPtrs& partials, DevState* st, DecideParams p, cudaStream_t s);
 cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int variant);
 int adam_ctas_per_sm(int variant);

@@ -97,6 +97,7 @@ class CDeviceState(C.Structure):
 
 
 EXPORTS = ["zero_plan_layout", "zero_init", "zero_buffer_sizes", "zero_bind_buffers", "zero_sim_group",
+           "zero_peer_export", "zero_peer_open",
            "zero_load_master", "zero_set_grad_ptrs", "zero_reduce_grads", "zero_step", "zero_gather_params",
            "zero_release_params", "zero_param_view", "zero_query", "zero_last_error", "zero_destroy",
            "zero_model_state_bytes", "zero_comm_elems_per_rank", "zero_abi_version"]
@@ -116,6 +117,8 @@ def _load():
         "zero_buffer_sizes": ([P, C.POINTER(CSizes)], C.c_int),
         "zero_bind_buffers": ([P, C.POINTER(CBuffers)], C.c_int),
         "zero_sim_group": ([C.POINTER(P), C.c_int], C.c_int),
+        "zero_peer_export": ([P, P, C.POINTER(C.c_size_t)], C.c_int),
+        "zero_peer_open": ([P, C.POINTER(P), C.c_size_t], C.c_int),
         "zero_load_master": ([P, C.POINTER(P)], C.c_int),
         "zero_set_grad_ptrs": ([P, C.POINTER(P)], C.c_int),
         "zero_reduce_grads": ([P, C.c_uint32, C.POINTER(P)], C.c_int),
@@ -290,6 +293,27 @@ class ZeroEngine:
             self.destroy()
         except Exception:
             pass
+
+    # -- cross-process PEER (CUDA IPC) --------------------------------------------
+    def peer_export(self) -> bytes:
+        n = C.c_size_t(0)
+        _check(lib.zero_peer_export(self._ctx, None, C.byref(n)), self._ctx)
+        buf = C.create_string_buffer(n.value)
+        _check(lib.zero_peer_export(self._ctx, buf, C.byref(n)), self._ctx)
+        return buf.raw[:n.value]
+
+    def peer_open(self, blobs: Sequence[bytes]):
+        bufs = [C.create_string_buffer(b, len(b)) for b in blobs]
+        arr = (C.c_void_p * len(bufs))(*[C.cast(b, C.c_void_p) for b in bufs])
+        _check(lib.zero_peer_open(self._ctx, arr, len(blobs[0])), self._ctx)
+
+    def link_peers(self, group=None):
+        """Exchange IPC blobs over a torch.distributed group and open them."""
+        import torch.distributed as dist
+        mine = self.peer_export()
+        allb = [None] * dist.get_world_size(group)
+        dist.all_gather_object(allb, mine, group=group)
+        self.peer_open(allb)
 
     # -- the four north-star calls and their helpers ---------------------------
     @staticmethod

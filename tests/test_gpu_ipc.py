@@ -1,0 +1,125 @@
+"""Cross-process PEER transport (CUDA IPC peer table + device-side release/acquire
+signals), exercised by 2 processes sharing one GPU: the same pull reduce-scatter /
+fused all-gather kernels as on an NVL8 box, with the ranks in separate processes
+and contexts.  Each rank's shard and replica must equal the replicated-DP oracle
+bit-exactly."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, stage, dt, q):
+    import sys
+    import traceback
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "tests")]
+    try:
+        import numpy as np
+        import torch.distributed as dist
+        import synth
+        from harness import bits16, bits32, zcfg_from_oracle
+        from oracle import layout as OL
+        from oracle import step as OS
+        from paper_1910_02054_b200 import ZeroEngine
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        ts = synth.mlp_layout((120, 90, 60, 30))
+        nl, ll = [t.numel for t in ts], [t.layer for t in ts]
+        cfg = OS.AdamConfig.defaults(dt)
+        cap = 1 << 12
+        e = ZeroEngine(nl, ll, world, rank, stage, zcfg_from_oracle(cfg), "peer", align=64, bucket_cap=cap)
+        e.link_peers()
+        masters = synth.master_values(ts, 1)
+        e.load_master([torch.from_numpy(a).cuda() for a in masters])
+        ost = OS.init_state(masters, cfg)
+        lay = OL.make_layout(nl, ll, world, 64, cap)
+        for s in range(4):
+            scale = ost.S if dt == "fp16" else 1.0
+            host = [synth.grads16(ts, 1, r, s, dt, scale=scale) for r in range(world)]
+            if s == 2:                       # overflow on rank 1 -> every rank skips the step
+                host[1][0] = host[1][0].clone()
+                host[1][0][5] = float("inf")
+            mine = [g.cuda() for g in host[rank]]
+            for k in reversed(range(e.info.n_buckets)):
+                e.reduce_grads(k, mine)
+            e.step()
+            info = e.step_info()
+            oinfo = OS.step(ost, [OS.grads_from_torch(h) for h in host], cfg)
+            assert info.overflow == int(oinfo.overflow) and info.t == oinfo.t, (s, info.overflow, info.t)
+            if not oinfo.overflow:
+                assert abs(info.grad_norm - oinfo.grad_norm) <= 1e-12 * oinfo.grad_norm
+        # this rank's shard against the oracle
+        spans = {}
+        for b in lay.buckets:
+            for p in b.pieces:
+                if p.tensor_off == 0:
+                    spans[p.tensor] = b.base + p.bucket_off
+
+        def flat(arrs, dtype):
+            out = np.zeros(lay.psi_padded, dtype)
+            for t, a in enumerate(arrs):
+                out[spans[t]:spans[t] + a.size] = a
+            return out
+
+        P32, M, V = e.shard()
+        for name, gpu, ref in (("p32", P32, ost.p32), ("m", M, ost.m), ("v", V, ost.v)):
+            rf = flat(ref, np.float32)
+            if stage == 0:
+                want = rf
+            else:
+                want = np.concatenate([rf[lo:hi] for lo, hi in (lay.owned_range(k, rank)
+                                                                for k in range(len(lay.buckets)))])
+            assert np.array_equal(bits32(gpu), want.view(np.uint32)), name
+        if stage in (0, 1, 2):
+            assert np.array_equal(bits16(e.p16_arena()), flat(ost.p16, np.uint16)), "replica"
+        else:
+            for L in range(4):
+                views = e.gather_params(L)
+                for t, v in views.items():
+                    assert np.array_equal(bits16(v), ost.p16[t]), ("gather", L, t)
+                e.release_params(L)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e.destroy()
+        dist.destroy_process_group()
+        q.put("ok")
+    except Exception:
+        q.put(traceback.format_exc())
+        raise
+
+
+@pytest.mark.parametrize("stage,dt", [(1, "bf16"), (2, "fp16"), (3, "bf16"), (0, "bf16")])
+def test_two_processes_one_gpu(stage, dt):
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, stage, dt, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+    hung = [p for p in procs if p.is_alive()]
+    for p in hung:
+        p.kill()
+        p.join(10)
+    msgs = []
+    while not q.empty():
+        msgs.append(q.get())
+    assert not hung, f"workers hung: {msgs}"
+    assert all(p.exitcode == 0 for p in procs) and msgs == ["ok", "ok"], msgs

@@ -43,7 +43,9 @@ def comm():
 @pytest.mark.parametrize("dt", ["bf16", "fp16"])
 @pytest.mark.parametrize("stage", [0, 1, 2, 3])
 def test_nccl_one_rank_matches_oracle(comm, dt, stage):
-    p = Pair(Run(synth.mlp_layout((300, 200, 100, 50)), 1, stage, OS.AdamConfig.defaults(dt), cap=1 << 13,
+    ts = synth.mlp_layout((300, 200, 100, 50))
+    n_layers = max(t.layer for t in ts) + 1
+    p = Pair(Run(ts, 1, stage, OS.AdamConfig.defaults(dt), cap=1 << 13,
                  inject=(2,), transport="nccl", nccl_comm=comm))
     for s in range(5):
         oi, gi = p.step()
@@ -54,7 +56,7 @@ def test_nccl_one_rank_matches_oracle(comm, dt, stage):
     assert c.steps == 5
     if stage == 3:
         e = p.engines[0]
-        for order in (range(4), reversed(range(4))):
+        for order in (range(n_layers), reversed(range(n_layers))):
             for L in order:
                 views = e.gather_params(L)
                 for t, v in views.items():
