@@ -129,6 +129,20 @@ __device__ __forceinline__ void h_set(U4& v, int j, uint32_t b) {
   else v.x[j >> 1] = (v.x[j >> 1] & 0xFFFF0000u) | b;
 }
 
+// acc += (double)u * (double)u with the fp32 -> fp64 widening done by integer ops for
+// normal u (exact: rebias the exponent, shift the significand), keeping the
+// conversion pipe (XU) free for the casts; zero, subnormal, inf and nan take cvt.
+__device__ __noinline__ double f32_to_f64_slow(float u) { return (double)u; }  // a real branch, not a predicated cvt
+__device__ __forceinline__ void sq_acc(double& acc, float u) {
+  const uint32_t b = __float_as_uint(u) & 0x7FFFFFFFu;
+  const uint32_t e = b >> 23;
+  double d;
+  if (e - 1u < 254u) d = __longlong_as_double(((uint64_t)b + (896ull << 23)) << 29);
+  else if (b == 0) d = 0.0;
+  else d = f32_to_f64_slow(u);
+  acc += d * d;
+}
+
 // ---------------------------------------------------------------------------
 // deterministic fp64 sum + OR flag over a grid (last-CTA combine)
 // ---------------------------------------------------------------------------
@@ -278,7 +292,7 @@ __global__ void __launch_bounds__(kThreads) k_flatten(const __grid_constant__ Fl
       if (a.epilogue) {
         flag |= D::nonfinite(b);
         const float u = __fmul_rn(D::widen(b), inv);
-        sumsq += (double)u * (double)u;
+        sq_acc(sumsq, u);
       }
     };
     auto emit8 = [&](uint32_t i, const float* x) {
@@ -290,12 +304,39 @@ __global__ void __launch_bounds__(kThreads) k_flatten(const __grid_constant__ Fl
         if (a.epilogue) {
           flag |= D::nonfinite(b);
           const float u = __fmul_rn(D::widen(b), inv);
-          sumsq += (double)u * (double)u;
+          sq_acc(sumsq, u);
         }
       }
       st128(dst + i, o);
     };
-    if (vec) {
+    if (vec && kCopy && S::kBytes == 2) {  // same dtype, sigma = 1: move the bits
+      const uint32_t nv = n & ~7u;
+#pragma unroll 1
+      for (uint32_t i0 = threadIdx.x * 8; i0 < nv; i0 += kThreads * 8 * V) {
+        U4 r[V];
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          const uint32_t i = i0 + u * kThreads * 8;
+          if (u == 0 || i < nv) r[u] = ld128(src + (uint64_t)i * 2);
+        }
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          const uint32_t i = i0 + u * kThreads * 8;
+          if (u == 0 || i < nv) {
+            st128(dst + i, r[u]);
+            if (a.epilogue) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const uint32_t b = h_get(r[u], j);
+                flag |= D::nonfinite(b);
+                sq_acc(sumsq, __fmul_rn(D::widen(b), inv));
+              }
+            }
+          }
+        }
+      }
+      for (uint32_t j = nv + threadIdx.x; j < n; j += kThreads) emit_one(j);
+    } else if (vec) {
       const uint32_t nv = n & ~7u;
 #pragma unroll 1
       for (uint32_t i0 = threadIdx.x * 8; i0 < nv; i0 += kThreads * 8 * V) {
@@ -462,7 +503,7 @@ __global__ void __launch_bounds__(T / 8 + 32, 1) k_flatten_tma(const __grid_cons
             if (a.epilogue) {
               flag |= D::nonfinite(b);
               const float u = __fmul_rn(D::widen(b), inv);
-              sumsq += (double)u * (double)u;
+              sq_acc(sumsq, u);
             }
           }
         }
@@ -565,7 +606,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
           o.x[j] = __float_as_uint(acc[j]);
           flag |= (uint32_t)!isfinite(acc[j]);
           const float u = __fmul_rn(acc[j], inv);
-          sumsq += (double)u * (double)u;
+          sq_acc(sumsq, u);
         }
         if (kReduce) st256(reinterpret_cast<float*>(a.dst) + i, o);
       } else {
@@ -576,7 +617,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
           h_set(o, j, b);
           flag |= D::nonfinite(b);
           const float u = __fmul_rn(D::widen(b), inv);
-          sumsq += (double)u * (double)u;
+          sq_acc(sumsq, u);
         }
         if (kReduce) st128(reinterpret_cast<uint16_t*>(a.dst) + i, o);
       }
@@ -604,7 +645,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
           if (kReduce) reinterpret_cast<uint16_t*>(a.dst)[k] = (uint16_t)b;
         }
         const float u = __fmul_rn(G, inv);
-        sumsq += (double)u * (double)u;
+        sq_acc(sumsq, u);
       }
     }
   }

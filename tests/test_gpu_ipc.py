@@ -89,7 +89,7 @@ def _worker(rank, world, port, stage, dt, q):
         if stage in (0, 1, 2):
             assert np.array_equal(bits16(e.p16_arena()), flat(ost.p16, np.uint16)), "replica"
         else:
-            for L in range(4):
+            for L in range(max(t.layer for t in ts) + 1):
                 views = e.gather_params(L)
                 for t, v in views.items():
                     assert np.array_equal(bits16(v), ost.p16[t]), ("gather", L, t)
