@@ -246,6 +246,9 @@ zero_status zero_set_grad_ptrs(struct zero_ctx* ctx, const void* const* tensor_g
  * so this rank holds the sum of its slice ("perform reduction on the entire
  * bucket at once") and the slice's overflow flag and norm partial.
  * tensor_grads: NULL (registered pointers) or an array of n_tensors device pointers.
+ * The gradient buffers are read asynchronously (LOCAL/NCCL flatten on library
+ * streams forked from the caller's stream) and are borrowed until zero_step is
+ * enqueued; the caller's stream is ordered after them by zero_step.
  * Errors: ZERO_EINVAL (bad k, missing pointer), ZERO_ESTATE (k already reduced this step). */
 zero_status zero_reduce_grads(struct zero_ctx* ctx, uint32_t bucket, const void* const* tensor_grads);
 

@@ -180,6 +180,16 @@ struct zero_ctx {
   DevState* st = nullptr;
   Slot* slots = nullptr;
   GridPartials* part_compute = nullptr;
+  GridPartials* part_flat2 = nullptr;
+  // LOCAL / NCCL: flattens of consecutive buckets alternate between two library streams
+  // forked from the caller's stream, so one bucket's tail overlaps the next one's
+  // start; they are joined into the step (zero_step) -- gradient buffers are
+  // therefore borrowed until zero_step is enqueued.
+  int n_flat_streams = 2;
+  cudaStream_t flat_stream[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  uint32_t flat_rr = 0;
+  bool flat_used[2] = {false, false};
   GridPartials* part_comm = nullptr;
   RankPartial* my_partial = nullptr;
   RankPartial* gathered = nullptr;
@@ -318,7 +328,8 @@ int grid_for(uint64_t work_items, int per_sm, int sms) {
 
 // bytes of the scratch arena and the offsets inside it
 struct ScratchLayout {
-  size_t st, slots, part_compute, part_comm, my_partial, gathered, segs, sig_flat, sig_rs, sig_part, sig_adam, total;
+  size_t st, slots, part_compute, part_flat2, part_comm, my_partial, gathered, segs, sig_flat, sig_rs, sig_part, sig_adam,
+      total;
 };
 // sig_flat[k][r] / sig_rs[k][r]: epoch at which rank r flattened / finished reducing bucket k
 // sig_part[r] / sig_adam[r]: epoch at which rank r published its partial / finished Adam
@@ -329,6 +340,7 @@ ScratchLayout scratch_layout(int n_slots, size_t n_segs, size_t n_buckets) {
   s.st = take(sizeof(DevState));
   s.slots = take(sizeof(Slot) * (size_t)std::max(n_slots, 1));
   s.part_compute = take(sizeof(GridPartials));
+  s.part_flat2 = take(sizeof(GridPartials));
   s.part_comm = take(sizeof(GridPartials));
   s.my_partial = take(sizeof(RankPartial));
   s.gathered = take(sizeof(RankPartial) * ZERO_MAX_RANKS);
@@ -563,6 +575,7 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   c->st = reinterpret_cast<DevState*>(s + sl.st);
   c->slots = reinterpret_cast<Slot*>(s + sl.slots);
   c->part_compute = reinterpret_cast<GridPartials*>(s + sl.part_compute);
+  c->part_flat2 = reinterpret_cast<GridPartials*>(s + sl.part_flat2);
   c->part_comm = reinterpret_cast<GridPartials*>(s + sl.part_comm);
   c->my_partial = reinterpret_cast<RankPartial*>(s + sl.my_partial);
   c->gathered = reinterpret_cast<RankPartial*>(s + sl.gathered);
@@ -591,6 +604,15 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
     for (auto& e : c->ev_pool_free) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   } else {
     c->comm_stream = c->stream;
+  }
+  if (const char* ev = getenv("ZERO_FLAT_STREAMS")) c->n_flat_streams = atoi(ev) >= 2 ? 2 : 1;
+  if (c->transport == ZERO_TRANSPORT_PEER) c->n_flat_streams = 1;  // peer paths stay on one stream
+  if (c->n_flat_streams == 2) {
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaStreamCreateWithFlags(&c->flat_stream[i], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   }
   CK(cudaEventCreateWithFlags(&c->ev_flat, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_step, cudaEventDisableTiming));
@@ -670,7 +692,7 @@ zero_status zero_set_grad_ptrs(zero_ctx* c, const void* const* g) {
 namespace {
 
 // issue the flatten of bucket k (compute stream).  epilogue at N_d == 1.
-zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads) {
+zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads, cudaStream_t fs, GridPartials* part) {
   const auto& tmpl = c->flat_tmpl[k];
   uint16_t* dst = c->flat_dst(k);
   const int ebytes = c->gdt == DT_F32 ? 4 : 2;
@@ -708,10 +730,10 @@ zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads) {
     a.dst = dst;
     a.sigma = c->cfg.grad_prescale;
     a.st = c->st;
-    a.part = c->part_compute;
+    a.part = part;
     a.slot = c->slots + slot;
-    if (tma_ok) CK(launch_flatten_tma(a, grid, c->stream, c->flat_tma));
-    else CK(launch_flatten(a, grid, c->stream, c->flat_vecs));
+    if (tma_ok) CK(launch_flatten_tma(a, grid, fs, c->flat_tma));
+    else CK(launch_flatten(a, grid, fs, c->flat_vecs));
     c->launches++;
   }
   return ZERO_OK;
@@ -772,8 +794,6 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
     if (pend >= 0 && c->group->flat_count[pend] < c->group->n)
       return c->fail(ZERO_ESTATE, "pool slot %u still holds bucket %d awaiting its reduce-scatter", ps, pend);
   }
-  if (pooled && c->transport == ZERO_TRANSPORT_NCCL) CK(cudaStreamWaitEvent(c->stream, c->ev_pool_free[ps], 0));
-
   if (c->cfg.timing && !c->step_open && c->ev_used < 4096) {
     zero_ctx::StepEvents* ev;
     zero_status es = c->timing_events(&ev);
@@ -781,7 +801,19 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
     CK(cudaEventRecord(ev->r0, c->stream));
     c->step_open = true;
   }
-  zero_status s = issue_flatten(c, k, grads);
+  // the stream this bucket is flattened on: the caller's, or one of two forked streams
+  cudaStream_t fs = c->stream;
+  GridPartials* fpart = c->part_compute;
+  if (c->n_flat_streams == 2) {
+    const int i = (int)(c->flat_rr++ & 1u);
+    fs = c->flat_stream[i];
+    fpart = i ? c->part_flat2 : c->part_compute;
+    CK(cudaEventRecord(c->ev_fork, c->stream));
+    CK(cudaStreamWaitEvent(fs, c->ev_fork, 0));
+    c->flat_used[i] = true;
+  }
+  if (pooled && c->transport == ZERO_TRANSPORT_NCCL) CK(cudaStreamWaitEvent(fs, c->ev_pool_free[ps], 0));
+  zero_status s = issue_flatten(c, k, grads, fs, fpart);
   if (s != ZERO_OK) return s;
 
   if (c->transport == ZERO_TRANSPORT_LOCAL) return finish_bucket_local(c, k);
@@ -876,8 +908,8 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
     return ZERO_OK;
   }
 
-  // NCCL: the compute stream produced the bucket; the comm stream reduces it
-  CK(cudaEventRecord(c->ev_flat, c->stream));
+  // NCCL: the flatten stream produced the bucket; the comm stream reduces it
+  CK(cudaEventRecord(c->ev_flat, fs));
   CK(cudaStreamWaitEvent(c->comm_stream, c->ev_flat, 0));
   const zero_bucket& b = c->buckets[k];
   const uint64_t sl = c->slice(k);
@@ -987,6 +1019,13 @@ zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
                    c->info.n_buckets);
   }
 
+  for (int i = 0; i < 2; ++i) {  // join the flatten streams into the step
+    if (!c->flat_used[i]) continue;
+    CK(cudaEventRecord(c->ev_join[i], c->flat_stream[i]));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_join[i], 0));
+    if (c->comm_stream != c->stream) CK(cudaStreamWaitEvent(c->stream, c->ev_join[i], 0));
+    c->flat_used[i] = false;
+  }
   zero_ctx::StepEvents* ev = nullptr;
   if (c->cfg.timing && c->step_open) {
     ev = &c->ev_pool[c->ev_used];
@@ -1467,6 +1506,14 @@ void zero_destroy(zero_ctx* c) {
     if (gs.ready) cudaEventDestroy(gs.ready);
     if (gs.freed) cudaEventDestroy(gs.freed);
   }
+  for (int i = 0; i < 2; ++i) {
+    if (c->flat_stream[i]) {
+      cudaStreamSynchronize(c->flat_stream[i]);
+      cudaStreamDestroy(c->flat_stream[i]);
+    }
+    if (c->ev_join[i]) cudaEventDestroy(c->ev_join[i]);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_flat) cudaEventDestroy(c->ev_flat);
   if (c->ev_step) cudaEventDestroy(c->ev_step);
   if (c->ev_tmp) cudaEventDestroy(c->ev_tmp);
