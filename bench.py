@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--cap", type=int, default=1 << 26)
     ap.add_argument("--align", type=int, default=64)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="N>1: peer = CUDA-IPC pull reduce-scatter + Adam-fused all-gather (default); nccl = library collectives")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -69,7 +71,8 @@ def ncu_traffic(kernel: str):
     try:
         with open(p) as f:
             d = json.load(f)
-        return d["kernels"][kernel]["dram_bytes_per_launch"], d["kernels"][kernel].get("elements")
+        k = d["kernels"][kernel]
+        return k["dram_bytes_per_launch"], k.get("elements")
     except Exception:
         return None, None
 
@@ -80,6 +83,8 @@ def max_over_ranks(value: float, device) -> float:
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return value
+    if dist.get_backend() == "gloo":
+        device = torch.device("cpu")
     t = torch.tensor([value], device=device, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -216,12 +221,22 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # ZERO_BENCH_SAME_DEVICE=1: every rank on cuda:0 (functional check of the N>1 flow on a
+    # 1-GPU box; the ranks time-slice the GPU, so its numbers are not throughput)
+    same_dev = os.environ.get("ZERO_BENCH_SAME_DEVICE") == "1"
+    if same_dev:
+        local = 0
+        if args.transport == "nccl":
+            raise SystemExit("NCCL cannot place two ranks on one GPU; use --transport peer")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        warm = torch.ones(1, device=dev)
-        dist.all_reduce(warm)
+        if same_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+            warm = torch.ones(1, device=dev)
+            dist.all_reduce(warm)
         torch.cuda.synchronize()
     stream = torch.cuda.current_stream(dev)
     tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float16
@@ -230,10 +245,12 @@ def main():
     if args.dtype == "fp16":
         cfg.loss_scale = 1.0        # inputs are generated unscaled; keep S fixed so no step overflows
         cfg.dynamic_loss_scale = False
-    transport = "local" if world == 1 else "nccl"
-    comm = nccl_comm_ptr(dist.group.WORLD) if world > 1 else 0
+    transport = "local" if world == 1 else args.transport
+    comm = nccl_comm_ptr(dist.group.WORLD) if world > 1 and transport == "nccl" else 0
     eng = ZeroEngine([t.numel for t in tensors], [t.layer for t in tensors], world, rank, args.stage, cfg,
                      transport, comm, stream, args.align, args.cap, dev)
+    if transport == "peer":
+        eng.link_peers(dist.new_group(backend="gloo"))   # exchange CUDA IPC handles, open the peer table
     info = eng.info
     nb = info.n_buckets
 
@@ -252,7 +269,7 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            dist.barrier() if same_dev else dist.barrier(device_ids=[local])
 
     for _ in range(max(args.warmup, 3)):
         one_step()
@@ -291,7 +308,9 @@ def main():
     adam_bytes = (24 + g_bytes + 2) * S_e     # p32, m, v read+write, G read, p16 write
     adam_ms = tm.adam_ms / max(tm.steps, 1)
     adam_gbs = adam_bytes / (adam_ms * 1e-3) / 1e9
-    traffic, _ = ncu_traffic("k_adam")
+    traffic, t_elems = ncu_traffic("k_adam")
+    if traffic is not None and t_elems:
+        traffic = traffic * S_e / t_elems   # the capture's bytes per element x this launch's elements
     reduce_ms = tm.reduce_ms / max(tm.steps, 1)
     pp = info.psi_padded
     # step roofline: sum over phases of max(HBM bytes / BW_HBM, NVLink bytes / BW_NVL)
@@ -376,7 +395,7 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.barrier(device_ids=[local])
+        barrier()
         dist.destroy_process_group()
 
 
