@@ -222,6 +222,8 @@ zero_status zero_sim_group(struct zero_ctx* const* ranks, int n);
  * pull reduce-scatter reads peers' buckets over NVLink, the Adam kernel stores the
  * recast parameters into every peer's replica (fused all-gather), and device-side
  * release/acquire signals at system scope order the ranks (no host barrier).
+ * As with NCCL, every rank must reduce the buckets of a step in the same order (the
+ * pull reduce-scatter of bucket k waits for every rank's flatten of bucket k).
  * zero_peer_export with blob == NULL returns the blob size in *blob_bytes.
  * Errors: ZERO_ESTATE (not an unlinked, bound PEER context), ZERO_EINVAL (a blob of
  * another rank/layout/stage), ZERO_ECUDA (IPC failure; the arenas must come from

@@ -38,6 +38,8 @@ def comm():
     dist.all_reduce(t)
     torch.cuda.synchronize()
     yield nccl_comm_ptr(dist.group.WORLD)
+    torch.cuda.synchronize()
+    dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("dt", ["bf16", "fp16"])
