@@ -262,9 +262,25 @@ def main():
     eng.set_grads(grads)
     torch.cuda.synchronize()
 
+    layer_ids = sorted({b.layer for b in eng.buckets})
+    layer_buckets = {L: [k for k, b in enumerate(eng.buckets) if b.layer == L] for L in layer_ids}
+
     def one_step():
-        for k in reversed(range(nb)):
-            eng.reduce_grads(k)
+        if args.stage == 3:
+            # SURVEY §8d step-only protocol for P_os+g+p: gather every layer for the
+            # forward (prefetching the next), then in reverse for the backward, each layer
+            # followed by its buckets' reduce-scatter; release after use
+            for L in layer_ids:
+                eng.gather_params(L)
+                eng.release_params(L)
+            for L in reversed(layer_ids):
+                eng.gather_params(L)
+                for k in reversed(layer_buckets[L]):
+                    eng.reduce_grads(k)
+                eng.release_params(L)
+        else:
+            for k in reversed(range(nb)):
+                eng.reduce_grads(k)
         eng.step()
 
     def barrier():
@@ -315,14 +331,18 @@ def main():
     pp = info.psi_padded
     # step roofline: sum over phases of max(HBM bytes / BW_HBM, NVLink bytes / BW_NVL)
     N = world
-    t_flat = 4 * pp / (hbm_peak * 1e9)
+    hbm = hbm_peak * 1e9
+    t_flat = 4 * pp / hbm
     if N == 1:
-        t_roof = t_flat + 28 * pp / (hbm_peak * 1e9)
+        t_roof = t_flat + 28 * pp / hbm
     else:
-        nvl = 2 * pp * (N - 1) / N / (NVLINK_GBS * 1e9)
-        t_rs = max((2 * pp + 2 * pp / N) / (hbm_peak * 1e9), nvl)
-        t_adam_ag = max((28 * pp / N + 2 * pp) / (hbm_peak * 1e9), nvl)
-        t_roof = t_flat + t_rs + t_adam_ag
+        nvl = 2 * pp * (N - 1) / N / (NVLINK_GBS * 1e9)      # one RS or one AG of Psi' 16-bit elements
+        if args.stage == 3:                                   # [AG fwd] -> [flatten + RS + AG bwd] -> [Adam]
+            t_roof = max(2 * pp / hbm, nvl) + max((4 * pp + 2 * pp + 2 * pp / N) / hbm, 2 * nvl) + 28 * pp / N / hbm
+        else:                                                 # [flatten] -> [RS] -> [Adam || AG]
+            t_rs = max((2 * pp + 2 * pp / N) / hbm, nvl)
+            t_adam_ag = max((28 * pp / N + 2 * pp) / hbm, nvl)
+            t_roof = t_flat + t_rs + t_adam_ag
     line = {
         "metric": METRIC, "value": value, "unit": "Gparams/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",

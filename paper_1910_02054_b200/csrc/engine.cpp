@@ -180,16 +180,17 @@ struct zero_ctx {
   DevState* st = nullptr;
   Slot* slots = nullptr;
   GridPartials* part_compute = nullptr;
-  GridPartials* part_flat2 = nullptr;
+  GridPartials* part_flat[4] = {};                 // grid partials per flatten stream
   // LOCAL / NCCL: flattens of consecutive buckets alternate between two library streams
   // forked from the caller's stream, so one bucket's tail overlaps the next one's
   // start; they are joined into the step (zero_step) -- gradient buffers are
   // therefore borrowed until zero_step is enqueued.
-  int n_flat_streams = 2;
-  cudaStream_t flat_stream[2] = {nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  static constexpr int kMaxFlatStreams = 4;
+  int n_flat_streams = 3;                          // ZERO_FLAT_STREAMS (1..4; 3 measured best)
+  cudaStream_t flat_stream[kMaxFlatStreams] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[kMaxFlatStreams] = {};
   uint32_t flat_rr = 0;
-  bool flat_used[2] = {false, false};
+  bool flat_used[kMaxFlatStreams] = {};
   GridPartials* part_comm = nullptr;
   RankPartial* my_partial = nullptr;
   RankPartial* gathered = nullptr;
@@ -328,7 +329,7 @@ int grid_for(uint64_t work_items, int per_sm, int sms) {
 
 // bytes of the scratch arena and the offsets inside it
 struct ScratchLayout {
-  size_t st, slots, part_compute, part_flat2, part_comm, my_partial, gathered, segs, sig_flat, sig_rs, sig_part, sig_adam,
+  size_t st, slots, part_compute, part_flat2, part_flat3, part_flat4, part_comm, my_partial, gathered, segs, sig_flat, sig_rs, sig_part, sig_adam,
       total;
 };
 // sig_flat[k][r] / sig_rs[k][r]: epoch at which rank r flattened / finished reducing bucket k
@@ -341,6 +342,8 @@ ScratchLayout scratch_layout(int n_slots, size_t n_segs, size_t n_buckets) {
   s.slots = take(sizeof(Slot) * (size_t)std::max(n_slots, 1));
   s.part_compute = take(sizeof(GridPartials));
   s.part_flat2 = take(sizeof(GridPartials));
+  s.part_flat3 = take(sizeof(GridPartials));
+  s.part_flat4 = take(sizeof(GridPartials));
   s.part_comm = take(sizeof(GridPartials));
   s.my_partial = take(sizeof(RankPartial));
   s.gathered = take(sizeof(RankPartial) * ZERO_MAX_RANKS);
@@ -575,7 +578,10 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   c->st = reinterpret_cast<DevState*>(s + sl.st);
   c->slots = reinterpret_cast<Slot*>(s + sl.slots);
   c->part_compute = reinterpret_cast<GridPartials*>(s + sl.part_compute);
-  c->part_flat2 = reinterpret_cast<GridPartials*>(s + sl.part_flat2);
+  c->part_flat[0] = c->part_compute;
+  c->part_flat[1] = reinterpret_cast<GridPartials*>(s + sl.part_flat2);
+  c->part_flat[2] = reinterpret_cast<GridPartials*>(s + sl.part_flat3);
+  c->part_flat[3] = reinterpret_cast<GridPartials*>(s + sl.part_flat4);
   c->part_comm = reinterpret_cast<GridPartials*>(s + sl.part_comm);
   c->my_partial = reinterpret_cast<RankPartial*>(s + sl.my_partial);
   c->gathered = reinterpret_cast<RankPartial*>(s + sl.gathered);
@@ -605,10 +611,11 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   } else {
     c->comm_stream = c->stream;
   }
-  if (const char* ev = getenv("ZERO_FLAT_STREAMS")) c->n_flat_streams = atoi(ev) >= 2 ? 2 : 1;
+  if (const char* ev = getenv("ZERO_FLAT_STREAMS"))
+    c->n_flat_streams = std::max(1, std::min(zero_ctx::kMaxFlatStreams, atoi(ev)));
   if (c->transport == ZERO_TRANSPORT_PEER) c->n_flat_streams = 1;  // peer paths stay on one stream
-  if (c->n_flat_streams == 2) {
-    for (int i = 0; i < 2; ++i) {
+  if (c->n_flat_streams > 1) {
+    for (int i = 0; i < c->n_flat_streams; ++i) {
       CK(cudaStreamCreateWithFlags(&c->flat_stream[i], cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming));
     }
@@ -804,10 +811,10 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
   // the stream this bucket is flattened on: the caller's, or one of two forked streams
   cudaStream_t fs = c->stream;
   GridPartials* fpart = c->part_compute;
-  if (c->n_flat_streams == 2) {
-    const int i = (int)(c->flat_rr++ & 1u);
+  if (c->n_flat_streams > 1) {
+    const int i = (int)(c->flat_rr++ % (uint32_t)c->n_flat_streams);
     fs = c->flat_stream[i];
-    fpart = i ? c->part_flat2 : c->part_compute;
+    fpart = c->part_flat[i];
     CK(cudaEventRecord(c->ev_fork, c->stream));
     CK(cudaStreamWaitEvent(fs, c->ev_fork, 0));
     c->flat_used[i] = true;
@@ -1019,7 +1026,7 @@ zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
                    c->info.n_buckets);
   }
 
-  for (int i = 0; i < 2; ++i) {  // join the flatten streams into the step
+  for (int i = 0; i < zero_ctx::kMaxFlatStreams; ++i) {  // join the flatten streams into the step
     if (!c->flat_used[i]) continue;
     CK(cudaEventRecord(c->ev_join[i], c->flat_stream[i]));
     CK(cudaStreamWaitEvent(c->comm_stream, c->ev_join[i], 0));
@@ -1506,7 +1513,7 @@ void zero_destroy(zero_ctx* c) {
     if (gs.ready) cudaEventDestroy(gs.ready);
     if (gs.freed) cudaEventDestroy(gs.freed);
   }
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < zero_ctx::kMaxFlatStreams; ++i) {
     if (c->flat_stream[i]) {
       cudaStreamSynchronize(c->flat_stream[i]);
       cudaStreamDestroy(c->flat_stream[i]);

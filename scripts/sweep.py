@@ -11,6 +11,7 @@ ap.add_argument("--adam", default="0,1,2,3,4")
 ap.add_argument("--flat", default="")          # e.g. "4x4,4x8"  (vecs x ctas)
 ap.add_argument("--base", default="")          # fixed env for every run, e.g. "ZERO_ADAM_VARIANT=1"
 ap.add_argument("--flat-tma", default="")      # e.g. "1,2,3,4"
+ap.add_argument("--flat-streams", default="")  # e.g. "1,2,3,4"
 args, extra = ap.parse_known_args()
 base = dict(kv.split("=") for kv in args.base.split(",") if kv)
 variants = []
@@ -19,6 +20,8 @@ for av in [x for x in args.adam.split(",") if x]:
 for fv in [x for x in args.flat.split(",") if x]:
     v, c = fv.split("x")
     variants.append(dict(base, ZERO_FLAT_VECS=v, ZERO_FLAT_CTAS=c))
+for fs in [x for x in args.flat_streams.split(",") if x]:
+    variants.append(dict(base, ZERO_FLAT_STREAMS=fs))
 for ft in [x for x in args.flat_tma.split(",") if x]:
     variants.append(dict(base, ZERO_FLAT_TMA=ft))
 for v in variants:
