@@ -254,10 +254,17 @@ def main():
     info = eng.info
     nb = info.n_buckets
 
-    masters = synth.gpu_masters(tensors, args.seed, dev)
-    eng.load_master(masters)
-    torch.cuda.synchronize()
-    del masters
+    # fp32 masters, loaded in chunks of <= 2^29 elements (bounded temporary memory)
+    chunk, cur = [], 0
+    for i, t in enumerate(tensors):
+        chunk.append(i)
+        cur += t.numel
+        if cur >= (1 << 29) or i == len(tensors) - 1:
+            masters = synth.gpu_masters(tensors, args.seed, dev, only=set(chunk))
+            eng.load_master(masters)
+            torch.cuda.synchronize()
+            del masters
+            chunk, cur = [], 0
     grad_buf, grads = synth.gpu_grads_flat(tensors, args.seed, rank, 0, tdt, dev)
     eng.set_grads(grads)
     torch.cuda.synchronize()

@@ -233,9 +233,12 @@ zero_status zero_peer_open(struct zero_ctx* ctx, const void* const* blobs, size_
 
 /* Initialise the model states from the full fp32 master weights: tensor_master[t]
  * is a device pointer to tensor t's numel fp32 values (every rank passes the same
- * values).  Writes this rank's fp32 shard, zeroes m and v, t = 0, and writes the
- * 16-bit parameters (full replica at stages 0-2, own shard at stage 3).
- * Pointers are borrowed until the call's stream work completes. */
+ * values), or NULL to leave tensor t as it is -- so a large model can be loaded in
+ * several calls with a bounded temporary (each call covers a subset of tensors).
+ * Writes this rank's fp32 shard of the given tensors and their 16-bit parameters
+ * (full replica at stages 0-2, own shard at stage 3); every call zeroes m and v and
+ * resets t, S and the loss-scale state.  Pointers are borrowed until the call's
+ * stream work completes. */
 zero_status zero_load_master(struct zero_ctx* ctx, const void* const* tensor_master);
 
 /* Register per-tensor gradient pointers (device; dtype = grad_dtype; tensor t has

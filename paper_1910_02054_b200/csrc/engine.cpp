@@ -652,14 +652,13 @@ zero_status zero_load_master(zero_ctx* c, const void* const* tensor_master) {
   STICKY(c);
   if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
   if (!tensor_master) return c->fail(ZERO_EINVAL, "tensor_master is NULL");
-  for (auto& p : c->pieces)
-    if (!tensor_master[p.tensor]) return c->fail(ZERO_EINVAL, "master pointer of tensor %u is NULL", p.tensor);
   CK(cudaMemsetAsync(c->m, 0, 8ull * c->opt_stride, c->stream));  // m and v are contiguous
   for (uint32_t k = 0; k < c->info.n_buckets; ++k) {
     const zero_bucket& b = c->buckets[k];
     const uint64_t sl = b.size / c->n_d;
     for (uint32_t j = 0; j < b.n_pieces; ++j) {
       const zero_piece& p = c->pieces[b.first_piece + j];
+      if (!tensor_master[p.tensor]) continue;  // loaded by another call (chunked init)
       LoadArgs a{};
       a.src = reinterpret_cast<const float*>(tensor_master[p.tensor]) + p.tensor_off;
       a.count = p.count;

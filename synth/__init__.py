@@ -237,12 +237,16 @@ def gpu_fill(out, key: int, start: int, scale: float, use_const: bool = False, c
         raise RuntimeError(f"synth_fill failed: cuda error {rc}")
 
 
-def gpu_masters(tensors: Sequence[TensorSpec], seed: int, device):
-    """fp32 master init on the device (same values as master_values)."""
+def gpu_masters(tensors: Sequence[TensorSpec], seed: int, device, only=None):
+    """fp32 master init on the device (same values as master_values); with `only`
+    (a set of tensor indices) the other entries are None."""
     import torch
     key = stream_key(seed, KIND_MASTER)
     out = []
-    for t, o in zip(tensors, tensor_offsets(tensors)):
+    for i, (t, o) in enumerate(zip(tensors, tensor_offsets(tensors))):
+        if only is not None and i not in only:
+            out.append(None)
+            continue
         a = torch.empty(t.numel, dtype=torch.float32, device=device)
         if t.role == ROLE_LNW:
             gpu_fill(a, key, o, 1.0, True, 1.0)

@@ -84,3 +84,70 @@ def test_backward_hooks_drive_the_step(stage):
     for t, a in enumerate(ost.p32):
         assert np.array_equal(bits32(P32[flat[t]:flat[t] + a.size]), a.view(np.uint32)), opt.names[t]
     opt.close()
+
+
+class TinyGPTUntied(torch.nn.Module):
+    """TinyGPT with its own output head (stage 3 needs every parameter used only
+    inside its layer module)."""
+
+    def __init__(self, vocab=512, h=128, n=3, seq=64):
+        super().__init__()
+        self.wte = torch.nn.Embedding(vocab, h)
+        self.wpe = torch.nn.Embedding(seq, h)
+        self.h = torch.nn.ModuleList([Block(h) for _ in range(n)])
+        self.head = torch.nn.Sequential(torch.nn.LayerNorm(h), torch.nn.Linear(h, vocab, bias=False))
+
+    def forward(self, idx):
+        x = self.wte(idx) + self.wpe(torch.arange(idx.shape[1], device=idx.device))
+        for b in self.h:
+            x = b(x)
+        return self.head(x)
+
+
+@pytest.mark.parametrize("n", [1, 2])
+def test_stage3_layer_hooks(n):
+    """P_os+g+p from torch: every layer module gathers its parameters before its
+    forward and again before its backward and releases them afterwards; n = 2 runs
+    two model replicas as the two ranks of a simulated group."""
+    from paper_1910_02054_b200 import ZeroConfig, ZeroSimGroup
+    from paper_1910_02054_b200.torch_zero import ZeroOptimizer, default_layer_of
+    torch.manual_seed(1)
+    base = TinyGPTUntied().cuda().to(torch.bfloat16)
+    models = [base] + [TinyGPTUntied().cuda().to(torch.bfloat16) for _ in range(n - 1)]
+    for m in models[1:]:
+        m.load_state_dict(base.state_dict())
+    init = [p.detach().float().cpu().numpy().reshape(-1).copy() for p in base.parameters()]
+    zc = ZeroConfig.defaults("bf16", pool_buckets=64)
+    if n == 1:
+        opts = [ZeroOptimizer(base, stage=3, config=zc, bucket_cap=1 << 15)]
+    else:
+        names = [nm for nm, _ in base.named_parameters()]
+        numels = [p.numel() for p in base.parameters()]
+        grp = ZeroSimGroup(numels, default_layer_of(names), n, 3, zc, 64, 1 << 15)
+        opts = [ZeroOptimizer(models[r], stage=3, config=zc, engine_factory=lambda nl, ll, r=r: grp[r])
+                for r in range(n)]
+    for p in base.parameters():
+        assert p.numel() == 0                     # only shards are resident between uses
+    cfg = OS.AdamConfig.defaults("bf16")
+    ost = OS.init_state(init, cfg)
+    for step in range(2):
+        grads = []
+        for r in range(n):
+            idx = torch.randint(0, 512, (2, 64), device="cuda")
+            loss = torch.nn.functional.cross_entropy(models[r](idx).float().view(-1, 512), idx.view(-1))
+            loss.backward()
+            grads.append(OS.grads_from_torch([p.grad.detach().reshape(-1).cpu() for p in opts[r].params]))
+            assert not opts[r]._gathered               # every layer released after its backward
+        for o in opts:
+            o.step()
+        OS.step(ost, grads, cfg)
+        assert opts[0].step_info().t == step + 1
+    # gather every layer and compare the 16-bit parameters with the oracle
+    for r in range(n):
+        o = opts[r]
+        for L in sorted(o._layer_tensors):
+            o._gather(L)
+            for t in o._layer_tensors[L]:
+                assert np.array_equal(bits16(o.params[t].detach().reshape(-1)), ost.p16[t]), (r, o.names[t])
+            o._release(L)
+    torch.cuda.synchronize()
