@@ -3,6 +3,7 @@
 // the paper; "c-k" are the readings in DESIGN.md §3.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -23,6 +24,13 @@ using namespace zero;
 namespace {
 
 thread_local std::string g_init_error;
+
+// NVTX range for the host-side issue of each phase (visible in nsys; header-only NVTX3,
+// a no-op unless a tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 int to_dt(zero_dtype d) { return d == ZERO_FP16 ? DT_F16 : d == ZERO_BF16 ? DT_BF16 : DT_F32; }
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
@@ -777,6 +785,7 @@ extern "C" {
 
 zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor_grads) {
   STICKY(c);
+  NvtxRange nvtx("zero_reduce_grads");
   if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
   if (k >= c->info.n_buckets) return c->fail(ZERO_EINVAL, "bucket %u out of range", k);
   if (c->reduced[k]) return c->fail(ZERO_ESTATE, "bucket %u already reduced this step", k);
@@ -1013,6 +1022,7 @@ extern "C" {
 
 zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
   STICKY(c);
+  NvtxRange nvtx("zero_step");
   if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
   ZeroGroup* g = c->group;
   if (g) {
@@ -1109,6 +1119,15 @@ zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
     CK(cudaStreamWaitEvent(c->stream, c->ev_step, 0));
   }
   c->counters.steps++;
+  if (c->stage == 3) {  // the step rewrote every shard: gathered copies are stale
+    for (auto& gs : c->gslots) {
+      gs.layer = -1;
+      gs.released = true;
+    }
+    std::fill(c->layer_slot.begin(), c->layer_slot.end(), -1);
+    c->last_layer = -1;
+    c->direction = +1;
+  }
   if (g) {
     c->stepped_this_round = true;
     if (++g->stepped == g->n) {
@@ -1323,6 +1342,7 @@ extern "C" {
 
 zero_status zero_gather_params(zero_ctx* c, uint32_t layer, void** views_out) {
   STICKY(c);
+  NvtxRange nvtx("zero_gather_params");
   if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
   if (c->stage != 3) return c->fail(ZERO_ESTATE, "zero_gather_params needs stage 3");
   auto it = c->layer_index.find(layer);

@@ -49,19 +49,19 @@ def test_nccl_one_rank_matches_oracle(comm, dt, stage):
     n_layers = max(t.layer for t in ts) + 1
     p = Pair(Run(ts, 1, stage, OS.AdamConfig.defaults(dt), cap=1 << 13,
                  inject=(2,), transport="nccl", nccl_comm=comm))
+    e = p.engines[0]
     for s in range(5):
         oi, gi = p.step()
         p.compare_info(oi, gi)
         assert oi.overflow == (s == 2)
+        if stage == 3:       # NCCL grouped layer gathers with prefetch, every step
+            for order in (range(n_layers), reversed(range(n_layers))):
+                for L in order:
+                    views = e.gather_params(L)
+                    for t, v in views.items():
+                        assert np.array_equal(v.cpu().view(torch.int16).numpy().view(np.uint16), p.ost.p16[t])
+                    e.release_params(L)
     p.compare()
-    c = p.engines[0].comm_counters()
+    c = e.comm_counters()
     assert c.steps == 5
-    if stage == 3:
-        e = p.engines[0]
-        for order in (range(n_layers), reversed(range(n_layers))):
-            for L in order:
-                views = e.gather_params(L)
-                for t, v in views.items():
-                    assert np.array_equal(v.cpu().view(torch.int16).numpy().view(np.uint16), p.ost.p16[t])
-                e.release_params(L)
     p.destroy()

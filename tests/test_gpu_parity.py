@@ -119,16 +119,17 @@ def test_loss_scale_sequence_on_device(golden):
 def test_stage3_gather_views_and_prefetch():
     ts = synth.mlp_layout((120, 80, 60, 40, 20))
     p = Pair(Run(ts, 4, 3, _cfg("bf16"), cap=1 << 12))
-    p.step()
     e = p.engines[2]
     n_layers = max(t.layer for t in ts) + 1
-    # forward then backward, releasing after use
-    for order in (range(n_layers), reversed(range(n_layers))):
-        for L in order:
-            views = e.gather_params(L)
-            for t, v in views.items():
-                assert np.array_equal(v.cpu().view(torch.int16).numpy().view(np.uint16), p.ost.p16[t])
-            e.release_params(L)
+    for _ in range(3):        # gathered copies must not survive a step (the shards change)
+        p.step()
+        # forward then backward, releasing after use
+        for order in (range(n_layers), reversed(range(n_layers))):
+            for L in order:
+                views = e.gather_params(L)
+                for t, v in views.items():
+                    assert np.array_equal(v.cpu().view(torch.int16).numpy().view(np.uint16), p.ost.p16[t])
+                e.release_params(L)
     torch.cuda.synchronize()
     c = e.comm_counters()
     assert c.all_gather > 0
