@@ -605,7 +605,7 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   if (const char* ev = getenv("ZERO_FLAT_VECS")) c->flat_vecs = atoi(ev);
   if (const char* ev = getenv("ZERO_FLAT_CTAS")) c->flat_ctas = atoi(ev);
   if (const char* ev = getenv("ZERO_FLAT_TMA")) c->flat_tma = atoi(ev);
-  if (c->flat_vecs != 1 && c->flat_vecs != 2 && c->flat_vecs != 4 && c->flat_vecs != 8) c->flat_vecs = 4;
+  if (c->flat_vecs != 2 && c->flat_vecs != 4 && c->flat_vecs != 8) c->flat_vecs = 4;
   if (c->flat_ctas < 1 || c->flat_ctas > 8) c->flat_ctas = 4;
 
   // streams and events

@@ -383,7 +383,6 @@ cudaError_t launch_flatten_v(const FlatArgs& a, int grid, cudaStream_t s) {
 
 cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s, int vecs) {
   switch (vecs) {
-    case 1: return launch_flatten_v<1>(a, grid, s);
     case 4: return launch_flatten_v<4>(a, grid, s);
     case 8: return launch_flatten_v<8>(a, grid, s);
     default: return launch_flatten_v<2>(a, grid, s);
@@ -533,8 +532,8 @@ cudaError_t launch_flatten_tma_t(const FlatArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// TMA flatten variants (T, STAGES): 1 = (4096, 4), 3 = (4096, 8), 4 = (2048, 8)
-// (measured slower than the register-staged k_flatten on B200: off by default)
+// TMA flatten (T 4096, 4 stages): measured 3.5 TB/s vs 4.2 TB/s for the register-staged
+// k_flatten on one stream (round-1 sweep), so it is off by default (ZERO_FLAT_TMA=1).
 template <int T, int STAGES>
 cudaError_t launch_flatten_tma_ts(const FlatArgs& a, int grid, cudaStream_t s) {
   const bool copy = (a.sigma == 1.0f) && (a.src_dtype == a.dst_dtype);
@@ -552,8 +551,6 @@ cudaError_t launch_flatten_tma_ts(const FlatArgs& a, int grid, cudaStream_t s) {
 
 cudaError_t launch_flatten_tma(const FlatArgs& a, int grid, cudaStream_t s, int variant) {
   switch (variant) {
-    case 3: return launch_flatten_tma_ts<4096, 8>(a, grid, s);
-    case 4: return launch_flatten_tma_ts<2048, 8>(a, grid, s);
     default: return launch_flatten_tma_ts<4096, 4>(a, grid, s);
   }
 }
@@ -1066,56 +1063,31 @@ cudaError_t launch_adam_tma_t(const AdamArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// variants: 0 = (2 CTAs/SM, U=1), 1 = (4, 1), 2 = (2, 2), 3 = (3, 1), 4 = (1, 4),
-// TMA (T elements per tile, T/8 consumer threads): 5 = (T 2048, 4 stages, 1 CTA/SM),
-// 6 = (1024, 6, 1), 7 = (1024, 4, 2 CTAs/SM), 8 = (2048, 6, 1), 9 = (2048, 3, 2),
-// 10 = (4096, 3, 1), 11 = (4096, 2, 1), 12 = (2048, 2, 3), 13 = (1024, 4, 3),
-// 14 = (6144, 2, 1), 15 = (3072, 2, 2), 16 = (2048, 2, 2), 17 = (4096, 1, 2), 18 = (2048, 4, 2)
+// Variants kept from the round-1 sweep (GPT-2 1.5B step on 1x B200, % of the measured
+// 6456.8 GB/s copy peak; profiles/r01_summary.md):
+//   0 = register-staged, 2 CTAs/SM (85.5 %)     1 = register-staged, 4 CTAs/SM, <= 64 regs (90.1 %)
+//   5 = TMA, T 2048 x 4 stages, 1 CTA/SM (92.6 %)   16 = TMA, 2048 x 2, 2 CTAs/SM (93.5 %)
+//  11 = TMA, T 4096 x 2 stages, 1 CTA/SM: 512 consumers + 1 producer warp (97.1-97.4 %, default)
+// (also measured and dropped: 1024x{4,6} 61-89 %, 2048x{3,6} 86-91 %, 4096x3 92 %, 6144x2 93 %,
+//  3072x2 92 %, 4096x1 70 %, register unroll-2 / 3 CTAs 81 %, 1 CTA unroll-4 87 %)
 int adam_ctas_per_sm(int variant) {
   switch (variant) {
     case 1: return 4;
-    case 3: return 3;
-    case 4: return 1;
     case 5: return 1;
-    case 6: return 1;
-    case 7: return 2;
-    case 8: return 1;
-    case 9: return 2;
-    case 10: return 1;
     case 11: return 1;
-    case 12: return 3;
-    case 13: return 3;
-    case 14: return 1;
-    case 15: return 2;
     case 16: return 2;
-    case 17: return 2;
-    case 18: return 2;
     default: return 2;
   }
 }
-bool adam_variant_is_tma(int variant) { return variant >= 5 && variant <= 18; }
+bool adam_variant_is_tma(int variant) { return variant == 5 || variant == 11 || variant == 16; }
 
 template <int PD, int GD>
 cudaError_t launch_adam_t(const AdamArgs& a, int grid, cudaStream_t s, int variant) {
   switch (variant) {
     case 5: return launch_adam_tma_t<PD, GD, 2048, 4>(a, grid, s);
-    case 6: return launch_adam_tma_t<PD, GD, 1024, 6>(a, grid, s);
-    case 7: return launch_adam_tma_t<PD, GD, 1024, 4>(a, grid, s);
-    case 8: return launch_adam_tma_t<PD, GD, 2048, 6>(a, grid, s);
-    case 9: return launch_adam_tma_t<PD, GD, 2048, 3>(a, grid, s);
-    case 10: return launch_adam_tma_t<PD, GD, 4096, 3>(a, grid, s);
     case 11: return launch_adam_tma_t<PD, GD, 4096, 2>(a, grid, s);
-    case 12: return launch_adam_tma_t<PD, GD, 2048, 2>(a, grid, s);
-    case 13: return launch_adam_tma_t<PD, GD, 1024, 4>(a, grid, s);
-    case 14: return launch_adam_tma_t<PD, GD, 6144, 2>(a, grid, s);
-    case 15: return launch_adam_tma_t<PD, GD, 3072, 2>(a, grid, s);
     case 16: return launch_adam_tma_t<PD, GD, 2048, 2>(a, grid, s);
-    case 17: return launch_adam_tma_t<PD, GD, 4096, 1>(a, grid, s);
-    case 18: return launch_adam_tma_t<PD, GD, 2048, 4>(a, grid, s);
     case 1: k_adam<PD, GD, 4, 1><<<grid, kThreads, 0, s>>>(a); break;
-    case 2: k_adam<PD, GD, 2, 2><<<grid, kThreads, 0, s>>>(a); break;
-    case 3: k_adam<PD, GD, 3, 1><<<grid, kThreads, 0, s>>>(a); break;
-    case 4: k_adam<PD, GD, 1, 4><<<grid, kThreads, 0, s>>>(a); break;
     default: k_adam<PD, GD, 2, 1><<<grid, kThreads, 0, s>>>(a); break;
   }
   return cudaGetLastError();
