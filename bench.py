@@ -192,8 +192,8 @@ def run_reference(args, tensors, psi_total):
         "metric": METRIC, "value": value, "unit": "Gparams/s", "n_gpus": args.gpus, "steps": steps,
         "warmup": warmup, "ms_per_step": dt / steps * 1e3 * psi_total / n, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.config, "stage": args.stage, "param_dtype": args.dtype, "psi": psi_total,
-                   "sample_params": n},
+        "config": {"workload": f"{args.config} layout, ZeRO stage {args.stage}", "psi": psi_total,
+                   "param_dtype": args.dtype, "sample_params": n},
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "Gparams/s", "cores": 1, "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": "Gparams/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -246,11 +246,32 @@ def main():
         cfg.loss_scale = 1.0        # inputs are generated unscaled; keep S fixed so no step overflows
         cfg.dynamic_loss_scale = False
     transport = "local" if world == 1 else args.transport
-    comm = nccl_comm_ptr(dist.group.WORLD) if world > 1 and transport == "nccl" else 0
-    eng = ZeroEngine([t.numel for t in tensors], [t.layer for t in tensors], world, rank, args.stage, cfg,
-                     transport, comm, stream, args.align, args.cap, dev)
-    if transport == "peer":
-        eng.link_peers(dist.new_group(backend="gloo"))   # exchange CUDA IPC handles, open the peer table
+    fallback_note = None
+
+    def make_engine(tr):
+        comm = nccl_comm_ptr(dist.group.WORLD) if tr == "nccl" else 0
+        e = ZeroEngine([t.numel for t in tensors], [t.layer for t in tensors], world, rank, args.stage, cfg,
+                       tr, comm, stream, args.align, args.cap, dev)
+        if tr == "peer":
+            e.link_peers(dist.new_group(backend="gloo"))   # exchange CUDA IPC handles, open the peer table
+        return e
+
+    try:
+        eng = make_engine(transport)
+        ok = 1
+    except Exception as exc:  # e.g. CUDA IPC not permitted in this container
+        eng, ok, fallback_note = None, 0, f"{transport} transport failed ({exc}); fell back to nccl"
+    if world > 1:                                           # every rank must agree on the transport
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev if not same_dev else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0 and transport != "nccl" and not same_dev:
+            if eng is not None:
+                eng.destroy()
+            fallback_note = fallback_note or "a peer rank failed to link; fell back to nccl"
+            transport = "nccl"
+            eng = make_engine("nccl")
+    if eng is None:
+        raise SystemExit(fallback_note)
     info = eng.info
     nb = info.n_buckets
 
@@ -358,6 +379,7 @@ def main():
                    "psi_padded": pp, "buckets": nb, "bucket_cap_elems": args.cap, "align_elems": args.align,
                    "param_dtype": args.dtype, "adam_state_dtype": "fp32", "reduce_mode": cfg.reduce_mode,
                    "transport": transport, "parallelism": f"zero{args.stage}-dp{world}",
+                   "transport_note": fallback_note,
                    "l2": "no flush: >= 25 GB streamed per step vs 126 MB L2"},
         "roofline": {"bound": "hbm", "kernel": "k_adam (fused partitioned Adam + recast)",
                      "achieved": adam_gbs, "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
