@@ -23,7 +23,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, stage, dt, q):
+def _worker(rank, world, port, stage, dt, mode, q):
     import sys
     import traceback
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -41,7 +41,7 @@ def _worker(rank, world, port, stage, dt, q):
         torch.cuda.set_device(0)
         ts = synth.mlp_layout((120, 90, 60, 30))
         nl, ll = [t.numel for t in ts], [t.layer for t in ts]
-        cfg = OS.AdamConfig.defaults(dt)
+        cfg = OS.AdamConfig.defaults(dt, reduce_mode=mode)
         cap = 1 << 12
         e = ZeroEngine(nl, ll, world, rank, stage, zcfg_from_oracle(cfg), "peer", align=64, bucket_cap=cap)
         e.link_peers()
@@ -104,12 +104,13 @@ def _worker(rank, world, port, stage, dt, q):
         raise
 
 
-@pytest.mark.parametrize("stage,dt", [(1, "bf16"), (2, "fp16"), (3, "bf16"), (0, "bf16")])
-def test_two_processes_one_gpu(stage, dt):
+@pytest.mark.parametrize("world,stage,dt,mode", [(2, 1, "bf16", "R16"), (2, 2, "fp16", "R16"), (2, 3, "bf16", "R16"),
+                                                 (2, 0, "bf16", "R16"), (3, 2, "bf16", "R32")])
+def test_processes_share_one_gpu(world, stage, dt, mode):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, stage, dt, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, stage, dt, mode, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
@@ -122,4 +123,4 @@ def test_two_processes_one_gpu(stage, dt):
     while not q.empty():
         msgs.append(q.get())
     assert not hung, f"workers hung: {msgs}"
-    assert all(p.exitcode == 0 for p in procs) and msgs == ["ok", "ok"], msgs
+    assert all(p.exitcode == 0 for p in procs) and msgs == ["ok"] * world, msgs
