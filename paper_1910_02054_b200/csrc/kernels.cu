@@ -508,6 +508,7 @@ __global__ void __launch_bounds__(T / 8 + 32, 1) k_flatten_tma(const __grid_cons
         }
         st128(dst_base + start + e, o);
       }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
@@ -1043,6 +1044,9 @@ __global__ void __launch_bounds__(T / 8 + 32, 1) k_adam_tma(const __grid_constan
         for (int d = 0; d < a.n_p16; ++d) st128(reinterpret_cast<uint16_t*>(a.p16[d]) + (i + pd), o);
       }
     }
+    // order this warp's generic-proxy reads of the stage before the next async-proxy
+    // (bulk copy) write into it, then release the stage to the producer
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
