@@ -110,3 +110,69 @@ def test_full_size_sampled(config, stage):
     eng.destroy()
     del eng, P32, M, V
     torch.cuda.empty_cache()
+
+
+def test_replicated_gradients_full_size_sim4():
+    """c-9 invariant at BASELINE config 2's full size: with every rank given the same
+    gradients, N_d = 4 simulated ranks (pull reduce-scatter + fused all-gather, stage 2)
+    must reproduce the N_d = 1 result bitwise (sum of 4 equal 16-bit values is exact,
+    1/(4S) is a power of two).  The N_d = 1 path itself is pinned to the oracle above."""
+    from paper_1910_02054_b200 import ZeroConfig, ZeroEngine, ZeroSimGroup
+    torch.cuda.empty_cache()
+    ts = synth.gpt2_1p5b()
+    nl, ll = [t.numel for t in ts], [t.layer for t in ts]
+    dev = torch.device("cuda", 0)
+    zc = ZeroConfig.defaults("bf16")
+    one = ZeroEngine(nl, ll, 1, 0, 2, zc, "local", align=64, bucket_cap=1 << 26, device=dev)
+    grp = ZeroSimGroup(nl, ll, 4, 2, zc, 64, 1 << 26)
+    for i in range(len(ts)):
+        m = synth.gpu_masters(ts, 1, dev, only={i})
+        one.load_master(m)
+        for e in grp.ranks:
+            e.load_master(m)
+    torch.cuda.synchronize()
+    for step in range(2):
+        buf, grads = synth.gpu_grads_flat(ts, 1, 0, step, torch.bfloat16, dev)
+        for k in reversed(range(one.info.n_buckets)):
+            one.reduce_grads(k, grads)
+        one.step()
+        for k in reversed(range(grp[0].info.n_buckets)):
+            for e in grp.ranks:
+                e.reduce_grads(k, grads)
+        for e in grp.ranks:
+            e.step()
+        torch.cuda.synchronize()
+        i1, i4 = one.step_info(), grp[0].step_info()
+        assert i1.t == i4.t == step + 1                         # norms: same sum, other fp64 order
+        assert abs(i1.grad_norm - i4.grad_norm) <= 1e-12 * i1.grad_norm
+        del buf, grads
+    # flat index -> (rank, local) for the N_d = 4 layout, compared bucket slice by bucket slice
+    P1, M1, V1 = one.shard()
+    flat1 = {}
+    for b in one.buckets:
+        for pc in one.pieces[b.first_piece:b.first_piece + b.n_pieces]:
+            if pc.tensor_off == 0:
+                flat1[pc.tensor] = b.base + pc.bucket_off
+    flat4 = {}
+    for b in grp[0].buckets:
+        for pc in grp[0].pieces[b.first_piece:b.first_piece + b.n_pieces]:
+            if pc.tensor_off == 0:
+                flat4[pc.tensor] = b.base + pc.bucket_off
+    shards = [e.shard() for e in grp.ranks]
+    full4 = [torch.empty(grp[0].info.psi_padded, dtype=torch.float32, device=dev) for _ in range(3)]
+    for k, b in enumerate(grp[0].buckets):
+        sl = b.size // 4
+        for r in range(4):
+            for w in range(3):
+                full4[w][b.base + r * sl:b.base + (r + 1) * sl] = shards[r][w][b.shard_off:b.shard_off + sl]
+    for t, spec in enumerate(ts):
+        a, c = flat1[t], flat4[t]
+        for w, one_arr in enumerate((P1, M1, V1)):
+            assert torch.equal(one_arr[a:a + spec.numel].view(torch.int32),
+                               full4[w][c:c + spec.numel].view(torch.int32)), (t, w)
+        for r in range(4):   # every rank's replica equals the N_d = 1 parameters
+            assert torch.equal(one.p16_arena()[a:a + spec.numel].view(torch.int16),
+                               grp[r].p16_arena()[c:c + spec.numel].view(torch.int16)), (t, r)
+    one.destroy()
+    grp.destroy()
+    torch.cuda.empty_cache()

@@ -169,3 +169,24 @@ def test_synth_gpu_fill_matches_host():
         host = torch.from_numpy(synth.uniform_pm1(key, 12345, n) * np.float32(2.0 ** 9)).to(tdt)
         assert torch.equal(out.cpu().view(torch.int16 if dt != "fp32" else torch.int32),
                            host.view(torch.int16 if dt != "fp32" else torch.int32))
+
+
+def test_long_run_dynamic_loss_scale():
+    """200 steps of config 1's MLP at N_d = 4 (fp16, dynamic scaling with a short
+    window so the scale doubles and halves many times; an overflow is injected every
+    37 steps): the device state machine and every state stay bit-exact."""
+    inject = tuple(range(5, 200, 37))
+    cfg = _cfg("fp16", scale_window=7, loss_scale=2.0 ** 12)
+    p = Pair(Run(synth.mlp_layout((400, 300, 200)), 4, 2, cfg, cap=1 << 14, inject=inject))
+    scales, overflows = set(), 0
+    for s in range(200):
+        oi, gi = p.step()
+        p.compare_info(oi, gi)
+        scales.add(gi[0].loss_scale)
+        overflows += oi.overflow
+        if s in inject:
+            assert oi.overflow
+    # the injected steps and the natural fp16 overflows once S grows are all skipped
+    assert len(scales) >= 4 and overflows >= len(inject) and p.ost.t == 200 - overflows
+    p.compare()
+    p.destroy()
