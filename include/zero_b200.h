@@ -241,6 +241,27 @@ zero_status zero_peer_open(struct zero_ctx* ctx, const void* const* blobs, size_
  * stream work completes. */
 zero_status zero_load_master(struct zero_ctx* ctx, const void* const* tensor_master);
 
+typedef struct {          /* loss-scale / Adam scalars (reading c-4) */
+  double b1t, b2t;
+  uint64_t t;
+  float loss_scale;
+  uint32_t good_steps;
+} zero_device_state;
+
+/* Checkpointing and resharding (P:357's partitions are per rank).
+ * zero_export_state writes the elements THIS rank owns of every tensor's fp32
+ * master / momentum / variance into the caller's per-tensor arrays (device pointers
+ * to numel fp32 each; NULL = skip), leaving the other elements untouched -- the
+ * union over ranks (e.g. a sum of zero-initialised arrays; at stage 0 any single
+ * rank) is the whole optimizer state in tensor coordinates, independent of N_d,
+ * bucketing and padding.  zero_import_state reads such arrays (the owned elements
+ * only; a context of any N_d/stage/C_B), rewrites the 16-bit parameters from the
+ * master, and, if st != NULL, sets the device scalars (t, beta^t, S, good steps; from
+ * zero_query(ZERO_Q_STATE)).  Both are stream-ordered on the compute stream. */
+zero_status zero_export_state(struct zero_ctx* ctx, void* const* master, void* const* m, void* const* v);
+zero_status zero_import_state(struct zero_ctx* ctx, const void* const* master, const void* const* m,
+                              const void* const* v, const zero_device_state* st);
+
 /* Register per-tensor gradient pointers (device; dtype = grad_dtype; tensor t has
  * numel contiguous elements).  Used by zero_reduce_grads when it is passed NULL. */
 zero_status zero_set_grad_ptrs(struct zero_ctx* ctx, const void* const* tensor_grads);
@@ -299,12 +320,6 @@ typedef struct {          /* persistent model-state bytes on this rank (Fig. 1 c
 typedef struct {          /* elements this rank sent, cumulative (S:173 CommStats) */
   uint64_t reduce_scatter, all_gather, all_reduce, steps;
 } zero_comm_counters;
-typedef struct {          /* loss-scale / Adam scalars (reading c-4) */
-  double b1t, b2t;
-  uint64_t t;
-  float loss_scale;
-  uint32_t good_steps;
-} zero_device_state;
 typedef struct {          /* device time per phase, CUDA events on the launching stream */
   double reduce_ms;       /* first flatten of a step -> last reduce-scatter/epilogue issued */
   double adam_ms;         /* the fused Adam kernel (sum over steps) */

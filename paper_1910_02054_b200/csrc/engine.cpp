@@ -694,6 +694,108 @@ zero_status zero_load_master(zero_ctx* c, const void* const* tensor_master) {
   return ZERO_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// the global range of bucket k this rank owns and its shard offset (stage 0: all of it)
+void owned_range(const zero_ctx* c, uint32_t k, uint64_t& lo, uint64_t& hi, uint64_t& local) {
+  const zero_bucket& b = c->buckets[k];
+  if (c->stage == 0) {
+    lo = b.base;
+    hi = b.base + b.size;
+    local = b.base;
+  } else {
+    const uint64_t sl = b.size / c->n_d;
+    lo = b.base + (uint64_t)c->rank * sl;
+    hi = lo + sl;
+    local = b.shard_off;
+  }
+}
+
+zero_status shard_io(zero_ctx* c, void* const* arrs, float* shard, int to_shard) {
+  for (uint32_t k = 0; k < c->info.n_buckets; ++k) {
+    const zero_bucket& b = c->buckets[k];
+    uint64_t lo, hi, local;
+    owned_range(c, k, lo, hi, local);
+    for (uint32_t j = 0; j < b.n_pieces; ++j) {
+      const zero_piece& p = c->pieces[b.first_piece + j];
+      if (!arrs[p.tensor]) continue;
+      ShardIOArgs a{};
+      a.tensor = reinterpret_cast<float*>(arrs[p.tensor]) + p.tensor_off;
+      a.shard = shard;
+      a.count = p.count;
+      a.flat_off = b.base + p.bucket_off;
+      a.own_lo = lo;
+      a.own_hi = hi;
+      a.local_base = local;
+      a.to_shard = to_shard;
+      CK(launch_shard_io(a, c->stream));
+      c->launches++;
+    }
+  }
+  return ZERO_OK;
+}
+}  // namespace
+
+extern "C" {
+
+zero_status zero_export_state(zero_ctx* c, void* const* master, void* const* m, void* const* v) {
+  STICKY(c);
+  if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
+  void* const* arrs[3] = {master, m, v};
+  float* shards[3] = {c->p32, c->m, c->v};
+  for (int i = 0; i < 3; ++i) {
+    if (!arrs[i]) continue;
+    zero_status s = shard_io(c, arrs[i], shards[i], 0);
+    if (s != ZERO_OK) return s;
+  }
+  return ZERO_OK;
+}
+
+zero_status zero_import_state(zero_ctx* c, const void* const* master, const void* const* m, const void* const* v,
+                              const zero_device_state* st) {
+  STICKY(c);
+  if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
+  if (st && !(st->loss_scale > 0.0f)) return c->fail(ZERO_EINVAL, "loss_scale must be > 0");
+  if (master) {  // owned fp32 elements + the 16-bit copy derived from them (as zero_load_master)
+    for (uint32_t k = 0; k < c->info.n_buckets; ++k) {
+      const zero_bucket& b = c->buckets[k];
+      uint64_t lo, hi, local;
+      owned_range(c, k, lo, hi, local);
+      for (uint32_t j = 0; j < b.n_pieces; ++j) {
+        const zero_piece& p = c->pieces[b.first_piece + j];
+        if (!master[p.tensor]) continue;
+        LoadArgs a{};
+        a.src = reinterpret_cast<const float*>(master[p.tensor]) + p.tensor_off;
+        a.count = p.count;
+        a.flat_off = b.base + p.bucket_off;
+        a.own_lo = lo;
+        a.own_hi = hi;
+        a.local_base = local;
+        a.p32 = c->p32;
+        a.p16 = c->p16;
+        a.p16_mode = c->stage == 3 ? 1 : 0;
+        a.p_dtype = c->pdt;
+        CK(launch_load(a, c->stream));
+        c->launches++;
+      }
+    }
+  }
+  const void* const* arrs[2] = {m, v};
+  float* shards[2] = {c->m, c->v};
+  for (int i = 0; i < 2; ++i) {
+    if (!arrs[i]) continue;
+    zero_status s = shard_io(c, const_cast<void* const*>(arrs[i]), shards[i], 1);
+    if (s != ZERO_OK) return s;
+  }
+  if (st) {
+    const float inv = (float)(1.0 / ((double)c->n_d * (double)st->loss_scale * (double)c->cfg.grad_prescale));
+    CK(launch_set_state(c->st, st->b1t, st->b2t, st->t, st->loss_scale, st->good_steps, inv, c->stream));
+    c->launches++;
+  }
+  return ZERO_OK;
+}
+
 zero_status zero_set_grad_ptrs(zero_ctx* c, const void* const* g) {
   STICKY(c);
   if (!g) return c->fail(ZERO_EINVAL, "null pointer array");

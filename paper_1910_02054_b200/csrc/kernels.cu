@@ -1194,6 +1194,45 @@ cudaError_t launch_push_partial(const PushArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// checkpoint / resharding support
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_shard_io(const __grid_constant__ ShardIOArgs a) {
+  for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < a.count; i += (uint64_t)gridDim.x * kThreads) {
+    const uint64_t g = a.flat_off + i;
+    if (g < a.own_lo || g >= a.own_hi) continue;
+    const uint64_t l = a.local_base + (g - a.own_lo);
+    if (a.to_shard) a.shard[l] = a.tensor[i];
+    else a.tensor[i] = a.shard[l];
+  }
+}
+cudaError_t launch_shard_io(const ShardIOArgs& a, cudaStream_t s) {
+  if (a.count == 0) return cudaSuccess;
+  const uint64_t blocks = (a.count + kThreads - 1) / kThreads;
+  k_shard_io<<<(int)(blocks < 4096 ? blocks : 4096), kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+__global__ void k_set_state(DevState* st, double b1t, double b2t, uint64_t t, float S, uint32_t good, float inv) {
+  st->b1t = b1t;
+  st->b2t = b2t;
+  st->t = t;
+  st->S = S;
+  st->good = good;
+  st->inv_cur = inv;
+  st->inv_adam = inv;
+  st->skip = 1u;
+  st->rec_t = t;
+  st->rec_overflow = 0;
+  st->rec_scale = S;
+  st->rec_clip = 1.0f;
+  st->rec_norm = 0.0;
+}
+cudaError_t launch_set_state(DevState* st, double b1t, double b2t, uint64_t t, float S, uint32_t good, float inv,
+                             cudaStream_t s) {
+  k_set_state<<<1, 1, 0, s>>>(st, b1t, b2t, t, S, good, inv);
+  return cudaGetLastError();
+}
+
 int sm_count() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);

@@ -138,6 +138,16 @@ struct LoadArgs {             // master init: fp32 piece -> shard / 16-bit copy
   int p_dtype;
 };
 
+struct ShardIOArgs {           // checkpoint: per-tensor fp32 piece <-> owned shard elements
+  float* tensor;              // the piece's first element in the per-tensor array
+  float* shard;               // p32, m or v
+  uint64_t count;
+  uint64_t flat_off;
+  uint64_t own_lo, own_hi;
+  uint64_t local_base;
+  int to_shard;               // 1: tensor -> shard, 0: shard -> tensor
+};
+
 // launchers (kernels.cu); return the launch error
 cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s, int vecs);
 cudaError_t launch_flatten_tma(const FlatArgs& a, int grid, cudaStream_t s, int variant);
@@ -176,6 +186,9 @@ bool adam_variant_is_tma(int variant);
 cudaError_t launch_copy(const CopyArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_load(const LoadArgs& a, cudaStream_t s);
 cudaError_t launch_init_state(DevState* st, float S, float inv, cudaStream_t s);
+cudaError_t launch_shard_io(const ShardIOArgs& a, cudaStream_t s);
+cudaError_t launch_set_state(DevState* st, double b1t, double b2t, uint64_t t, float S, uint32_t good, float inv,
+                             cudaStream_t s);
 int sm_count();
 
 }  // namespace zero

@@ -97,7 +97,7 @@ class CDeviceState(C.Structure):
 
 
 EXPORTS = ["zero_plan_layout", "zero_init", "zero_buffer_sizes", "zero_bind_buffers", "zero_sim_group",
-           "zero_peer_export", "zero_peer_open",
+           "zero_peer_export", "zero_peer_open", "zero_export_state", "zero_import_state",
            "zero_load_master", "zero_set_grad_ptrs", "zero_reduce_grads", "zero_step", "zero_gather_params",
            "zero_release_params", "zero_param_view", "zero_query", "zero_last_error", "zero_destroy",
            "zero_model_state_bytes", "zero_comm_elems_per_rank", "zero_abi_version"]
@@ -119,6 +119,8 @@ def _load():
         "zero_sim_group": ([C.POINTER(P), C.c_int], C.c_int),
         "zero_peer_export": ([P, P, C.POINTER(C.c_size_t)], C.c_int),
         "zero_peer_open": ([P, C.POINTER(P), C.c_size_t], C.c_int),
+        "zero_export_state": ([P, C.POINTER(P), C.POINTER(P), C.POINTER(P)], C.c_int),
+        "zero_import_state": ([P, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(CDeviceState)], C.c_int),
         "zero_load_master": ([P, C.POINTER(P)], C.c_int),
         "zero_set_grad_ptrs": ([P, C.POINTER(P)], C.c_int),
         "zero_reduce_grads": ([P, C.c_uint32, C.POINTER(P)], C.c_int),
@@ -380,6 +382,31 @@ class ZeroEngine:
     def p16_arena(self) -> torch.Tensor:
         return self.arenas["p16"].view(_TORCH_DT[self.config.param_dtype])
 
+    # -- checkpointing / resharding ----------------------------------------------
+    def export_state(self) -> dict:
+        """This rank's optimizer state in tensor coordinates: {"master", "m", "v"} per-tensor
+        fp32 tensors holding the elements this rank owns (zeros elsewhere) + the device
+        scalars.  Combine ranks with `consolidate_states`."""
+        dev = self.device
+        out = {k: [torch.zeros(n, dtype=torch.float32, device=dev) for n in self.numels] for k in ("master", "m", "v")}
+        arrs = [self._ptr_array(out[k]) for k in ("master", "m", "v")]
+        _check(lib.zero_export_state(self._ctx, *arrs), self._ctx)
+        st = self.device_state()      # synchronizes
+        out["scalars"] = {"b1t": st.b1t, "b2t": st.b2t, "t": st.t, "loss_scale": st.loss_scale,
+                          "good_steps": st.good_steps}
+        out["stage"] = self.stage
+        return out
+
+    def import_state(self, state: dict):
+        """Load a state in tensor coordinates (from any N_d / stage / C_B)."""
+        keep = [[t.float().contiguous() for t in state[k]] for k in ("master", "m", "v")]
+        arrs = [self._ptr_array(k) for k in keep]
+        sc = state["scalars"]
+        st = CDeviceState(sc["b1t"], sc["b2t"], sc["t"], sc["loss_scale"], sc["good_steps"])
+        _check(lib.zero_import_state(self._ctx, *arrs, C.byref(st)), self._ctx)
+        torch.cuda.synchronize(self.device)
+        del keep
+
     # -- queries --------------------------------------------------------------
     def memory(self) -> CMemory:
         out = CMemory()
@@ -401,6 +428,18 @@ class ZeroEngine:
         out = CDeviceState()
         _check(lib.zero_query(self._ctx, Q_STATE, C.byref(out), C.sizeof(out)), self._ctx)
         return out
+
+
+def consolidate_states(states: Sequence[dict]) -> dict:
+    """Merge the per-rank `export_state` dicts of one job into the full optimizer state
+    (owned elements are disjoint across ranks at stages 1-3; at stage 0 every rank
+    holds everything)."""
+    if states[0].get("stage") == 0:
+        return states[0]
+    out = {k: [sum(st[k][t] for st in states) for t in range(len(states[0][k]))] for k in ("master", "m", "v")}
+    out["scalars"] = dict(states[0]["scalars"])
+    out["stage"] = states[0].get("stage")
+    return out
 
 
 class ZeroSimGroup:
