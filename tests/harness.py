@@ -45,6 +45,8 @@ class Run:
     inject: Sequence[int] = ()          # steps (0-based) with +inf at rank min(1,n-1), flat index Psi//2
     transport: str = "local"            # n == 1: "local" or "nccl" (1-rank communicator)
     nccl_comm: int = 0
+    pool: int = 2                       # C_B staging slots (stages 2/3, N_d > 1)
+    prefetch: int = 1                   # stage-3 prefetch depth
 
 
 class Pair:
@@ -58,6 +60,8 @@ class Pair:
         self.layers = [t.layer for t in ts]
         self.lay = OL.make_layout(self.numels, self.layers, run.n, run.align, run.cap)
         zc = zcfg_from_oracle(run.cfg)
+        zc.pool_buckets = run.pool
+        zc.prefetch_depth = run.prefetch
         if run.n == 1:
             self.engines = [ZeroEngine(self.numels, self.layers, 1, 0, run.stage, zc, run.transport,
                                        nccl_comm=run.nccl_comm, align=run.align, bucket_cap=run.cap)]

@@ -105,7 +105,8 @@ def _worker(rank, world, port, stage, dt, mode, q):
 
 
 @pytest.mark.parametrize("world,stage,dt,mode", [(2, 1, "bf16", "R16"), (2, 2, "fp16", "R16"), (2, 3, "bf16", "R16"),
-                                                 (2, 0, "bf16", "R16"), (3, 2, "bf16", "R32")])
+                                                 (2, 0, "bf16", "R16"), (3, 2, "bf16", "R32"),
+                                                 (4, 3, "fp16", "R16")])
 def test_processes_share_one_gpu(world, stage, dt, mode):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
@@ -114,7 +115,7 @@ def test_processes_share_one_gpu(world, stage, dt, mode):
     for p in procs:
         p.start()
     for p in procs:
-        p.join(180)
+        p.join(300)
     hung = [p for p in procs if p.is_alive()]
     for p in hung:
         p.kill()
