@@ -195,6 +195,7 @@ struct zero_ctx {
   // therefore borrowed until zero_step is enqueued.
   static constexpr int kMaxFlatStreams = 4;
   int n_flat_streams = 3;                          // ZERO_FLAT_STREAMS (1..4; 3 measured best)
+  int n_flat_streams_req = 3;
   cudaStream_t flat_stream[kMaxFlatStreams] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxFlatStreams] = {};
   uint32_t flat_rr = 0;
@@ -362,6 +363,17 @@ ScratchLayout scratch_layout(int n_slots, size_t n_segs, size_t n_buckets) {
   s.sig_adam = take(sizeof(uint64_t) * ZERO_MAX_RANKS);
   s.total = o;
   return s;
+}
+
+zero_status create_flat_streams(zero_ctx* c) {
+  if (c->n_flat_streams <= 1) return ZERO_OK;
+  for (int i = 0; i < c->n_flat_streams; ++i) {
+    if (c->flat_stream[i]) continue;
+    CK(cudaStreamCreateWithFlags(&c->flat_stream[i], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming));
+  }
+  if (!c->ev_fork) CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  return ZERO_OK;
 }
 
 }  // namespace
@@ -621,14 +633,12 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   }
   if (const char* ev = getenv("ZERO_FLAT_STREAMS"))
     c->n_flat_streams = std::max(1, std::min(zero_ctx::kMaxFlatStreams, atoi(ev)));
-  if (c->transport == ZERO_TRANSPORT_PEER) c->n_flat_streams = 1;  // peer paths stay on one stream
-  if (c->n_flat_streams > 1) {
-    for (int i = 0; i < c->n_flat_streams; ++i) {
-      CK(cudaStreamCreateWithFlags(&c->flat_stream[i], cudaStreamNonBlocking));
-      CK(cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming));
-    }
-    CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
-  }
+  c->n_flat_streams_req = c->n_flat_streams;
+  // simulated PEER ranks share one stream (host-ordered collectives); zero_peer_open
+  // switches a cross-process PEER context to forked flatten streams + a comm stream
+  if (c->transport == ZERO_TRANSPORT_PEER) c->n_flat_streams = 1;
+  zero_status fs_status = create_flat_streams(c);
+  if (fs_status != ZERO_OK) return fs_status;
   CK(cudaEventCreateWithFlags(&c->ev_flat, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_step, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_tmp, cudaEventDisableTiming));
@@ -898,14 +908,6 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
   // C_B pool slot reuse (stages 2/3, N_d > 1)
   const bool pooled = c->stage >= 2 && c->transport != ZERO_TRANSPORT_LOCAL;
   const uint32_t ps = pooled ? k % c->pool : 0;
-  if (pooled && c->ipc) {  // every peer finished reading this slot's previous bucket
-    const auto& pl = c->pool_last[ps];
-    if (pl.first >= 0) {
-      WaitArgs w{c->sig(c->rank, c->off_sig_rs, (size_t)pl.first * ZERO_MAX_RANKS), c->n_d, pl.second};
-      CK(launch_wait(w, c->stream));
-      c->launches++;
-    }
-  }
   if (pooled && c->transport == ZERO_TRANSPORT_PEER && c->group) {
     const int pend = c->pool_pending[ps];
     if (pend >= 0 && c->group->flat_count[pend] < c->group->n)
@@ -930,6 +932,14 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
     c->flat_used[i] = true;
   }
   if (pooled && c->transport == ZERO_TRANSPORT_NCCL) CK(cudaStreamWaitEvent(fs, c->ev_pool_free[ps], 0));
+  if (pooled && c->ipc) {  // every peer finished reading this slot's previous bucket
+    const auto& pl = c->pool_last[ps];
+    if (pl.first >= 0) {
+      WaitArgs w{c->sig(c->rank, c->off_sig_rs, (size_t)pl.first * ZERO_MAX_RANKS), c->n_d, pl.second};
+      CK(launch_wait(w, fs));
+      c->launches++;
+    }
+  }
   zero_status s = issue_flatten(c, k, grads, fs, fpart);
   if (s != ZERO_OK) return s;
 
@@ -942,8 +952,12 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
     for (int j = 0; j < c->n_d; ++j) sa.dst[j] = c->sig(j, c->off_sig_flat, kk + c->rank);
     sa.n = c->n_d;
     sa.epoch = ep;
-    CK(launch_signal(sa, c->stream));
+    CK(launch_signal(sa, fs));
     c->launches++;
+    // the reduce-scatter starts only after the local flatten (a host-side stream
+    // dependency), so its CTAs spin only on remote ranks' flatten signals
+    CK(cudaEventRecord(c->ev_flat, fs));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_flat, 0));
     const uint64_t sl = c->slice(k);
     const size_t foff = (size_t)(c->flat_dst(k) - c->grad);
     RSArgs a{};
@@ -962,12 +976,12 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
     a.st = c->st;
     a.part = c->part_comm;
     a.slot = c->slots + c->slot_base[k];
-    CK(launch_reduce_scatter(a, grid_for((sl + 2047) / 2048, 4, c->sms), c->stream));
+    CK(launch_reduce_scatter(a, grid_for((sl + 2047) / 2048, 4, c->sms), c->comm_stream));
     c->launches++;
     c->counters.reduce_scatter += sl * (uint64_t)(c->n_d - 1);
     if (c->stage == 0) {  // all-reduce = RS + AG of the reduced slices
       WaitArgs w{c->sig(c->rank, c->off_sig_rs, kk), c->n_d, ep};
-      CK(launch_wait(w, c->stream));
+      CK(launch_wait(w, c->comm_stream));
       c->launches++;
       CopyArgs ca{};
       const zero_bucket& b = c->buckets[k];
@@ -977,7 +991,7 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
       }
       ca.count = sl;
       ca.n = c->n_d;
-      CK(launch_copy(ca, grid_for((sl + 2047) / 2048, 2, c->sms), c->stream));
+      CK(launch_copy(ca, grid_for((sl + 2047) / 2048, 2, c->sms), c->comm_stream));
       c->launches++;
       c->counters.all_gather += sl * (uint64_t)(c->n_d - 1);
     }
@@ -1353,7 +1367,16 @@ zero_status zero_peer_open(zero_ctx* c, const void* const* blobs, size_t blob_by
     c->peer_scratch[r] = reinterpret_cast<char*>(mapped[2]);
   }
   c->ipc = true;
-  return ZERO_OK;
+  // cross-process: the pull reduce-scatter (NVLink-bound) runs on its own stream so it
+  // overlaps the next buckets' flattens (HBM-bound) on the forked flatten streams
+  if (c->comm_stream == c->stream) {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
+    c->own_comm_stream = true;
+  }
+  c->n_flat_streams = c->n_flat_streams_req;
+  return create_flat_streams(c);
 }
 
 zero_status zero_sim_group(zero_ctx* const* ranks, int n) {
