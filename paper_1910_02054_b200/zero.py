@@ -16,7 +16,8 @@ from typing import Dict, List, Optional, Sequence
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "libzero_b200.so")
+# ZERO_LIB_PATH: load another build of the same ABI (A/B kernel experiments)
+_LIB_PATH = os.environ.get("ZERO_LIB_PATH") or os.path.join(_PKG, "libzero_b200.so")
 
 # ---------------------------------------------------------------------------
 # ABI structs (mirror include/zero_b200.h field by field)
