@@ -251,7 +251,7 @@ struct SrcLoad<DT_F32> {
 // contiguous slice [b*per_cta, (b+1)*per_cta) of that range, walking the pieces it
 // overlaps; each thread keeps V 128-bit loads in flight.
 template <int SDT, int DDT, bool kCopy, int V>
-__global__ void __launch_bounds__(kThreads) k_flatten(const __grid_constant__ FlatArgs a) {
+__global__ void __launch_bounds__(kThreads, 6) k_flatten(const __grid_constant__ FlatArgs a) {  // <= 40 regs: +1 % (A/B)
   using S = SrcLoad<SDT>;
   using D = H16<DDT>;
   const float sigma = a.sigma;
