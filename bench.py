@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="N>1: peer = CUDA-IPC pull reduce-scatter + Adam-fused all-gather (default); nccl = library collectives")
     ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--graph", action="store_true",
+                    help="capture one whole step (all zero_reduce_grads + zero_step) in a CUDA graph and time replays")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
@@ -238,10 +240,13 @@ def main():
             warm = torch.ones(1, device=dev)
             dist.all_reduce(warm)
         torch.cuda.synchronize()
-    stream = torch.cuda.current_stream(dev)
+    # the graph mode captures on a side stream (capture is not allowed on the legacy stream)
+    stream = torch.cuda.Stream(dev) if args.graph else torch.cuda.current_stream(dev)
+    torch.cuda.set_stream(stream)
     tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float16
 
-    cfg = ZeroConfig.defaults(args.dtype, timing=True)
+    # phase events cannot be timed inside a captured graph: --graph runs without them
+    cfg = ZeroConfig.defaults(args.dtype, timing=not args.graph)
     if args.dtype == "fp16":
         cfg.loss_scale = 1.0        # inputs are generated unscaled; keep S fixed so no step overflows
         cfg.dynamic_loss_scale = False
@@ -321,6 +326,17 @@ def main():
     barrier()
     eng.timing()                           # reset the phase accumulators
     launches0 = eng.timing().kernel_launches
+    graph, launches_per_step = None, None
+    if args.graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            one_step()
+        launches_per_step = eng.timing().kernel_launches - launches0
+        for _ in range(2):
+            graph.replay()
+        torch.cuda.synchronize()
+        barrier()
+    run_step = graph.replay if graph is not None else one_step
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -331,7 +347,7 @@ def main():
     clocks.mark(True)
     ev0.record(stream)
     for _ in range(args.steps):
-        one_step()
+        run_step()
     ev1.record(stream)
     torch.cuda.synchronize()
     clocks.mark(False)
@@ -339,7 +355,7 @@ def main():
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, dev)
     clk = clocks.stop()
     tm = eng.timing()
-    gpu_launches = tm.kernel_launches - launches0
+    gpu_launches = tm.kernel_launches - launches0 if graph is None else launches_per_step * args.steps
     info_rec = eng.step_info()
     assert info_rec.overflow == 0 and info_rec.t >= args.steps, "benchmark steps must not be skipped"
 
@@ -350,12 +366,12 @@ def main():
     S_e = info.psi_padded if args.stage == 0 else info.shard
     g_bytes = 4 if (cfg.reduce_mode == "R32" and world > 1) else 2
     adam_bytes = (24 + g_bytes + 2) * S_e     # p32, m, v read+write, G read, p16 write
-    adam_ms = tm.adam_ms / max(tm.steps, 1)
-    adam_gbs = adam_bytes / (adam_ms * 1e-3) / 1e9
+    adam_ms = tm.adam_ms / tm.steps if tm.steps else None
+    adam_gbs = adam_bytes / (adam_ms * 1e-3) / 1e9 if adam_ms else None
     traffic, t_elems = ncu_traffic("k_adam")
     if traffic is not None and t_elems:
         traffic = traffic * S_e / t_elems   # the capture's bytes per element x this launch's elements
-    reduce_ms = tm.reduce_ms / max(tm.steps, 1)
+    reduce_ms = tm.reduce_ms / tm.steps if tm.steps else None
     pp = info.psi_padded
     # step roofline: sum over phases of max(HBM bytes / BW_HBM, NVLink bytes / BW_NVL)
     N = world
@@ -383,12 +399,14 @@ def main():
                    "l2": "no flush: >= 25 GB streamed per step vs 126 MB L2"},
         "roofline": {"bound": "hbm", "kernel": "k_adam (fused partitioned Adam + recast)",
                      "achieved": adam_gbs, "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": adam_gbs / hbm_peak, "traffic": traffic,
+                     "frac": adam_gbs / hbm_peak if adam_gbs else None, "traffic": traffic,
                      "bytes_per_launch": adam_bytes, "ms_per_launch": adam_ms,
-                     "share_of_step": adam_ms / ms},
+                     "share_of_step": adam_ms / ms if adam_ms else None,
+                     "note": None if adam_ms else "--graph: per-kernel events are not recorded inside the graph"},
         "step_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
                           "reduce_phase_ms": reduce_ms, "flatten_gbs": 4 * pp / (reduce_ms * 1e-3) / 1e9
-                          if N == 1 else None},
+                          if (N == 1 and reduce_ms) else None},
+        "cuda_graph": bool(graph is not None),
         "clocks": clk,
         "gpu_launches": int(gpu_launches),
     }
