@@ -58,7 +58,7 @@ class ZeroOptimizer:
                  n_d: int = 1, rank: int = 0, transport: str = "local", nccl_comm: int = 0,
                  layer_of: Optional[Callable[[Sequence[str]], List[int]]] = None,
                  bucket_cap: int = 1 << 26, align: int = 64, stream: Optional[torch.cuda.Stream] = None,
-                 engine_factory=None):
+                 engine_factory=None, process_group=None):
         if stage not in (0, 1, 2, 3):
             raise ValueError("stage must be 0..3")
         named = [(n, p) for n, p in model.named_parameters() if p.requires_grad]
@@ -80,6 +80,8 @@ class ZeroOptimizer:
         else:
             self.engine = ZeroEngine([p.numel() for p in self.params], layers, n_d, rank, stage, self.config,
                                      transport, nccl_comm, stream, align, bucket_cap, self.params[0].device)
+            if transport == "peer" and n_d > 1:   # one process per rank: open the CUDA-IPC peer table
+                self.engine.link_peers(process_group)
         self.shapes = [p.shape for p in self.params]
         # fp32 masters from the model's current weights
         masters = [p.detach().float().contiguous().view(-1) for p in self.params]

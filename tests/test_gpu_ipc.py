@@ -125,3 +125,81 @@ def test_processes_share_one_gpu(world, stage, dt, mode):
         msgs.append(q.get())
     assert not hung, f"workers hung: {msgs}"
     assert all(p.exitcode == 0 for p in procs) and msgs == ["ok"] * world, msgs
+
+
+def _torch_worker(rank, world, port, stage, q):
+    import sys
+    import traceback
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "tests")]
+    try:
+        import numpy as np
+        import torch.distributed as dist
+        from harness import bits16
+        from oracle import step as OS
+        from paper_1910_02054_b200 import ZeroConfig
+        from paper_1910_02054_b200.torch_zero import ZeroOptimizer
+        from test_gpu_torch_zero import TinyGPTUntied
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        torch.manual_seed(3)                       # same initial weights on every rank
+        model = TinyGPTUntied().cuda().to(torch.bfloat16)
+        init = [p.detach().float().cpu().numpy().reshape(-1).copy() for p in model.parameters()]
+        opt = ZeroOptimizer(model, stage=stage, config=ZeroConfig.defaults("bf16"), n_d=world, rank=rank,
+                            transport="peer", bucket_cap=1 << 14)
+        cfg = OS.AdamConfig.defaults("bf16")
+        ost = OS.init_state(init, cfg)
+        g = torch.Generator(device="cpu").manual_seed(100 + rank)   # each rank its own data
+        for step in range(3):
+            idx = torch.randint(0, 512, (2, 64), generator=g).cuda()
+            loss = torch.nn.functional.cross_entropy(model(idx).float().view(-1, 512), idx.view(-1))
+            loss.backward()
+            mine = [p.grad.detach().reshape(-1).cpu() for p in opt.params]
+            everyone = [None] * world
+            dist.all_gather_object(everyone, mine)
+            opt.step()
+            OS.step(ost, [OS.grads_from_torch(gs) for gs in everyone], cfg)
+        torch.cuda.synchronize()
+        if stage < 3:
+            for t, p in enumerate(opt.params):
+                assert np.array_equal(bits16(p.detach().reshape(-1)), ost.p16[t]), opt.names[t]
+        else:
+            for L in sorted(opt._layer_tensors):
+                opt._gather(L)
+                for t in opt._layer_tensors[L]:
+                    assert np.array_equal(bits16(opt.params[t].detach().reshape(-1)), ost.p16[t]), opt.names[t]
+                opt._release(L)
+        torch.cuda.synchronize()
+        dist.barrier()
+        opt.close()
+        dist.destroy_process_group()
+        q.put("ok")
+    except Exception:
+        q.put(traceback.format_exc())
+        raise
+
+
+@pytest.mark.parametrize("stage", [2, 3])
+def test_torch_training_across_processes(stage):
+    """Two processes, one model replica each, ZeroOptimizer over the CUDA-IPC peer
+    transport: real autograd hooks drive the cross-process pull reduce-scatter,
+    the fused all-gather (stage 2) or the per-layer gathers (stage 3); every rank's
+    parameters equal replicated-DP Adam on both ranks' gradients."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _port()
+    procs = [ctx.Process(target=_torch_worker, args=(r, 2, port, stage, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+    hung = [p for p in procs if p.is_alive()]
+    for p in hung:
+        p.kill()
+        p.join(10)
+    msgs = []
+    while not q.empty():
+        msgs.append(q.get())
+    assert not hung, f"workers hung: {msgs}"
+    assert all(p.exitcode == 0 for p in procs) and msgs == ["ok", "ok"], msgs
