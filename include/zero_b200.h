@@ -171,10 +171,14 @@ struct zero_ctx;
  *  stage: 0 = replicated DP (all-reduce, every rank updates all Psi'),
  *         1 = P_os, 2 = P_os+g, 3 = P_os+g+p.
  *  K: optimizer bytes per parameter; must be 12 ("Mixed-precision Adam has K=12").
- *  transport: LOCAL requires n_d == 1; NCCL requires nccl_comm (an ncclComm_t of
- *  size n_d whose rank is `rank`, borrowed, never destroyed); PEER requires a later
- *  zero_sim_group.  compute_stream: cudaStream_t (borrowed; NULL = legacy default).
- *  The current CUDA device is the context's device.
+ *  transport: LOCAL requires n_d == 1 (n_d == 1 with PEER also becomes LOCAL);
+ *  NCCL requires nccl_comm (an ncclComm_t of size n_d whose rank is `rank`, borrowed,
+ *  never destroyed; n_d == 1 keeps the NCCL code path on a 1-rank communicator);
+ *  PEER requires a later zero_sim_group (one process) or zero_peer_open (CUDA IPC).
+ *  compute_stream: cudaStream_t (borrowed; NULL = legacy default stream).
+ *  The current CUDA device is the context's device.  No device work happens here
+ *  (the host layout and arena sizes are usable without a GPU); the context owns only
+ *  host memory until zero_bind_buffers.
  *  Errors: ZERO_EINVAL (K != 12, stage not in 0..3, bad dtype combination,
  *  rank/n_d/transport mismatch, layout errors), ZERO_EUNSUPPORTED (R32 with the
  *  NCCL transport, stage 0 with R32), ZERO_ECUDA. */
@@ -188,10 +192,10 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
  *                     (S_e = Psi'/N_d; Psi' at stage 0)            -- K Psi / N_d
  *  p16     2 * Psi' (stages 0-2: full replica) or 2 * Psi'/N_d (stage 3 shard)
  *  grad    2 * Psi' (stages 0/1: flat gradient buffer, reduced in place) or
- *          pool_buckets * max B_k * 2 (stages 2/3 staging pool, N_d > 1); 0 otherwise
+ *          pool_buckets * max B_k * 2 (stages 2/3 staging pool, NCCL/PEER); 0 otherwise
  *  gred    reduced-gradient shard: stages 2/3 R16 2*Psi'/N_d, R32 4*Psi'/N_d;
  *          stage 1 R32 4*Psi'/N_d; 0 otherwise
- *  gather  stage 3, N_d > 1: (prefetch_depth + 1) * max layer elements * 2
+ *  gather  stage 3, NCCL/PEER: (prefetch_depth + 1) * max layer elements * 2
  *  scratch device state, norm slots, partial sums, segment table (< 1 MB)
  * The grad/gred/gather/scratch arenas are the only transient buffers: nothing is
  * allocated during a step (M_D). */
@@ -283,8 +287,15 @@ zero_status zero_reduce_grads(struct zero_ctx* ctx, uint32_t bucket, const void*
  * the all-gather buffer, then the all-gather (stages 1/2, "all-gather ... at
  * the end of each training step"; stage 0 updates everything locally; stage 3
  * keeps only the shard).  host_out (optional, pinned host memory for
- * asynchrony) receives the step record when the step's work completes.
- * Errors: ZERO_ESTATE if some bucket of the step was not reduced. */
+ * asynchrony) receives the step record when the step's work completes (read it
+ * after synchronizing the compute stream).  An overflow skips the update on the
+ * device (t, m, v, master unchanged; the loss scale is halved when dynamic); the host
+ * never waits.  The caller's compute stream is ordered after the step; with the
+ * cross-process PEER transport the step ends with a device barrier, so every
+ * replica is final before any rank's next forward.  Stage 3 copies gathered before
+ * the step are invalidated (the next zero_gather_params gathers again).
+ * Errors: ZERO_ESTATE if some bucket of the step was not reduced (or, in a
+ * simulated group, not reduced by every rank; or the rank already stepped). */
 zero_status zero_step(struct zero_ctx* ctx, zero_step_info* host_out);
 
 /* Stage 3: make layer `layer`'s 16-bit parameters available (all-gather of its
@@ -299,7 +310,10 @@ zero_status zero_step(struct zero_ctx* ctx, zero_step_info* host_out);
 zero_status zero_gather_params(struct zero_ctx* ctx, uint32_t layer, void** views_out);
 zero_status zero_release_params(struct zero_ctx* ctx, uint32_t layer);
 
-/* Stages 0-2: device pointer of tensor t's 16-bit parameters in the replica. */
+/* Stages 0-2 (and stage 3 at LOCAL): device pointer of tensor t's 16-bit parameters
+ * in the replica (contiguous numel elements; rewritten by every zero_step).
+ * Errors: ZERO_EINVAL (bad tensor / zero-size tensor), ZERO_ESTATE (not bound, or
+ * stage 3 with a collective transport: use zero_gather_params). */
 zero_status zero_param_view(const struct zero_ctx* ctx, uint32_t tensor, void** p16);
 
 /* Synchronous queries (they synchronize the compute stream when device data is read). */
@@ -330,8 +344,13 @@ typedef struct {          /* device time per phase, CUDA events on the launching
 } zero_timing;
 zero_status zero_query(const struct zero_ctx* ctx, int what, void* out, size_t out_bytes);
 
-/* Last error text of ctx (NULL: of the calling thread's last failed zero_init). */
+/* Last error text of ctx (NULL: of the calling thread's last failed zero_init or
+ * zero_plan_layout).  The string is owned by the library and valid until the next
+ * call on the same context. */
 const char* zero_last_error(const struct zero_ctx* ctx);
+/* Synchronize the context's streams, close IPC mappings, destroy the library's
+ * streams and events and free the context.  The caller's arenas are not freed.
+ * Destroying one member of a simulated group dissolves the group. */
 void zero_destroy(struct zero_ctx* ctx);
 
 /* Pure host functions (no GPU): the closed forms the runtime reports against. */
