@@ -120,7 +120,8 @@ class ZeroOptimizer:
                 self._bucket_tensors[pc.bucket].append(pc.tensor)
                 self._tensor_buckets[pc.tensor].append(pc.bucket)
         self._remaining = [len(ts) for ts in self._bucket_tensors]
-        self._ptrs = [None] * len(self.params)
+        self._ptrs = [None] * len(self.params)          # keeps the grads alive until step()
+        self._parr = self.engine.pointer_array()         # the same pointers for the C call
         self._layer_of_tensor = list(layers)
         self._handles = [p.register_post_accumulate_grad_hook(self._make_hook(t)) for t, p in enumerate(self.params)]
         self.reduced_order: List[int] = []
@@ -133,10 +134,11 @@ class ZeroOptimizer:
             if not g.is_contiguous():
                 p.grad = g = g.contiguous()
             self._ptrs[t] = g
+            self._parr[t] = g.data_ptr()
             for k in self._tensor_buckets[t]:
                 self._remaining[k] -= 1
                 if self._remaining[k] == 0:
-                    self.engine.reduce_grads(k, self._ptrs)
+                    self.engine.reduce_grads(k, self._parr)
                     self.reduced_order.append(k)
             if self.stage == 3:
                 L = self._layer_of_tensor[t]

@@ -331,9 +331,18 @@ class ZeroEngine:
         self._grad_keep = list(grads)
         _check(lib.zero_set_grad_ptrs(self._ctx, self._ptr_array(grads)), self._ctx)
 
-    def reduce_grads(self, bucket: int, grads: Optional[Sequence[torch.Tensor]] = None):
-        arr = self._ptr_array(grads) if grads is not None else None
+    def reduce_grads(self, bucket: int, grads=None):
+        """grads: None (registered pointers), a sequence of tensors (or None) per tensor,
+        or a prebuilt ctypes pointer array (see `pointer_array`)."""
+        if grads is None or isinstance(grads, C.Array):
+            arr = grads
+        else:
+            arr = self._ptr_array(grads)
         _check(lib.zero_reduce_grads(self._ctx, bucket, arr), self._ctx)
+
+    def pointer_array(self):
+        """A reusable per-tensor pointer array for reduce_grads (fill entries in place)."""
+        return (C.c_void_p * len(self.numels))()
 
     def step(self):
         """Enqueue zero_step; the record lands in pinned memory (read with step_info())."""
