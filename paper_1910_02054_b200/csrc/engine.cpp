@@ -217,7 +217,7 @@ struct zero_ctx {
   std::vector<int> pool_pending;                   // per pool slot: bucket awaiting its RS (-1 none)
   std::vector<const void*> grad_ptrs;
   std::vector<cudaEvent_t> ev_pool_free;           // NCCL: RS of the slot's last bucket done
-  cudaEvent_t ev_flat = nullptr, ev_step = nullptr, ev_tmp = nullptr;
+  cudaEvent_t ev_flat = nullptr, ev_step = nullptr;
   bool stepped_this_round = false;
 
   // stage 3
@@ -641,7 +641,6 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   if (fs_status != ZERO_OK) return fs_status;
   CK(cudaEventCreateWithFlags(&c->ev_flat, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_step, cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&c->ev_tmp, cudaEventDisableTiming));
   if (c->stage == 3) {
     c->gslots.resize(c->cfg.prefetch_depth + 1);
     for (auto& g : c->gslots) {
@@ -1667,7 +1666,6 @@ void zero_destroy(zero_ctx* c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_flat) cudaEventDestroy(c->ev_flat);
   if (c->ev_step) cudaEventDestroy(c->ev_step);
-  if (c->ev_tmp) cudaEventDestroy(c->ev_tmp);
   if (c->own_comm_stream && c->comm_stream) cudaStreamDestroy(c->comm_stream);
   delete c;
 }
