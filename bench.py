@@ -343,16 +343,20 @@ def main():
     time.sleep(0.3)
     barrier()
     torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     clocks.mark(True)
-    ev0.record(stream)
-    for _ in range(args.steps):
+    evs[0].record(stream)
+    for i in range(args.steps):
         run_step()
-    ev1.record(stream)
+        evs[i + 1].record(stream)      # per-step boundaries (median / p10 / p90)
     torch.cuda.synchronize()
     clocks.mark(False)
     barrier()
-    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, dev)
+    ms = max_over_ranks(evs[0].elapsed_time(evs[-1]) / args.steps, dev)
+    per_step = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps))
+
+    def pct(q):
+        return per_step[min(len(per_step) - 1, int(q * (len(per_step) - 1) + 0.5))]
     clk = clocks.stop()
     tm = eng.timing()
     gpu_launches = tm.kernel_launches - launches0 if graph is None else launches_per_step * args.steps
@@ -389,7 +393,9 @@ def main():
             t_roof = t_flat + t_rs + t_adam_ag
     line = {
         "metric": METRIC, "value": value, "unit": "Gparams/s", "n_gpus": world, "steps": args.steps,
-        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "warmup": max(args.warmup, 3), "ms_per_step": ms,
+        "ms_per_step_p10_p50_p90": [pct(0.1), pct(0.5), pct(0.9)] if world == 1 else None,
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.config} layout, ZeRO stage {args.stage}", "psi": psi_total,
                    "psi_padded": pp, "buckets": nb, "bucket_cap_elems": args.cap, "align_elems": args.align,
