@@ -561,9 +561,40 @@ cudaError_t launch_flatten_tma(const FlatArgs& a, int grid, cudaStream_t s, int 
 // ascending rank, one rounding for R16), fused with the overflow flag and the
 // norm partial.  reduce == 0: epilogue only (slice already reduced by NCCL).
 // ---------------------------------------------------------------------------
-template <int DT, bool kR32, bool kReduce, bool kVec>
+// NR: number of ranks known at compile time (2, 4, 8; 0 = a.n at run time).  U: 8-element
+// groups per thread per iteration, so that U*NR 128-bit loads are in flight before the
+// sums (NVLink latency is ~2 us: the pull needs many bytes in flight per SM).
+template <int DT, bool kR32>
+__device__ __forceinline__ void rs_emit8(const RSArgs& a, uint64_t i, const float (&acc)[8], bool store, float inv,
+                                         double& sumsq, uint32_t& flag) {
+  using D = H16<DT>;
+  if (kR32) {
+    U8 o;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      o.x[j] = __float_as_uint(acc[j]);
+      flag |= (uint32_t)!isfinite(acc[j]);
+      sq_acc(sumsq, __fmul_rn(acc[j], inv));
+    }
+    if (store) st256(reinterpret_cast<float*>(a.dst) + i, o);
+  } else {
+    U4 o;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t b = D::narrow(acc[j]);
+      h_set(o, j, b);
+      flag |= D::nonfinite(b);
+      sq_acc(sumsq, __fmul_rn(D::widen(b), inv));
+    }
+    if (store) st128(reinterpret_cast<uint16_t*>(a.dst) + i, o);
+  }
+}
+
+template <int DT, bool kR32, bool kReduce, bool kVec, int NR, int U>
 __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_constant__ RSArgs a) {
   using D = H16<DT>;
+  constexpr int R = NR > 0 ? NR : kMaxRanks;
+  const int n = NR > 0 ? NR : a.n;
   if (a.wait_flags) {  // every rank has flattened this bucket (cross-process PEER)
     if (threadIdx.x == 0) wait_all(a.wait_flags, a.n, a.epoch);
     __syncthreads();
@@ -571,61 +602,92 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
   const float inv = a.st->inv_cur;
   double sumsq = 0.0;
   uint32_t flag = 0;
-  const uint64_t stride = (uint64_t)gridDim.x * kThreads * (kVec ? 8 : 1);
-  for (uint64_t i = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) * (kVec ? 8 : 1); i < a.count; i += stride) {
-    if (kVec && i + 8 <= a.count) {
-      float acc[8];
+  const uint64_t step = (uint64_t)kThreads * (kVec ? 8 : 1);
+  const uint64_t stride = (uint64_t)gridDim.x * step * (kVec ? U : 1);
+  for (uint64_t i0 = ((uint64_t)blockIdx.x * kThreads * (kVec ? U : 1) + threadIdx.x) * (kVec ? 8 : 1); i0 < a.count;
+       i0 += stride) {
+    if (kVec && i0 + 8 <= a.count) {
       if (kReduce) {
-        U4 v[kMaxRanks];
+        U4 v[U][R];
 #pragma unroll
-        for (int r = 0; r < kMaxRanks; ++r)
-          if (r < a.n) v[r] = ld128(reinterpret_cast<const uint16_t*>(a.src[r]) + i);
+        for (int u = 0; u < U; ++u) {
+          const uint64_t i = i0 + (uint64_t)u * step;
+          if (u == 0 || i + 8 <= a.count) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = D::widen(h_get(v[0], j));
-#pragma unroll
-        for (int r = 1; r < kMaxRanks; ++r)
-          if (r < a.n) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], D::widen(h_get(v[r], j)));
+            for (int r = 0; r < R; ++r)
+              if (NR > 0 || r < n) v[u][r] = ld128(reinterpret_cast<const uint16_t*>(a.src[r]) + i);
           }
-      } else if (kR32) {
-        U8 w = ld256(reinterpret_cast<const float*>(a.dst) + i);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = __uint_as_float(w.x[j]);
-      } else {
-        U4 w = ld128(reinterpret_cast<const uint16_t*>(a.dst) + i);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = D::widen(h_get(w, j));
-      }
-      if (kR32) {
-        U8 o;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          o.x[j] = __float_as_uint(acc[j]);
-          flag |= (uint32_t)!isfinite(acc[j]);
-          const float u = __fmul_rn(acc[j], inv);
-          sq_acc(sumsq, u);
         }
-        if (kReduce) st256(reinterpret_cast<float*>(a.dst) + i, o);
-      } else {
-        U4 o;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t b = kReduce ? D::narrow(acc[j]) : D::narrow(acc[j]);
-          h_set(o, j, b);
-          flag |= D::nonfinite(b);
-          const float u = __fmul_rn(D::widen(b), inv);
-          sq_acc(sumsq, u);
+        for (int u = 0; u < U; ++u) {
+          const uint64_t i = i0 + (uint64_t)u * step;
+          if (u == 0 || i + 8 <= a.count) {
+            float acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = D::widen(h_get(v[u][0], j));
+#pragma unroll
+            for (int r = 1; r < R; ++r)
+              if (NR > 0 || r < n) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], D::widen(h_get(v[u][r], j)));
+              }
+            rs_emit8<DT, kR32>(a, i, acc, true, inv, sumsq, flag);
+          } else if (i < a.count) {
+            for (uint64_t k = i; k < a.count; ++k) {   // ragged tail of the second group
+              float acc = D::widen(reinterpret_cast<const uint16_t*>(a.src[0])[k]);
+              for (int r = 1; r < n; ++r) acc = __fadd_rn(acc, D::widen(reinterpret_cast<const uint16_t*>(a.src[r])[k]));
+              if (kR32) {
+                flag |= (uint32_t)!isfinite(acc);
+                reinterpret_cast<float*>(a.dst)[k] = acc;
+                sq_acc(sumsq, __fmul_rn(acc, inv));
+              } else {
+                const uint32_t b = D::narrow(acc);
+                flag |= D::nonfinite(b);
+                reinterpret_cast<uint16_t*>(a.dst)[k] = (uint16_t)b;
+                sq_acc(sumsq, __fmul_rn(D::widen(b), inv));
+              }
+            }
+          }
         }
-        if (kReduce) st128(reinterpret_cast<uint16_t*>(a.dst) + i, o);
+      } else {  // epilogue only over the (NCCL-)reduced slice
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint64_t i = i0 + (uint64_t)u * step;
+          if (!(u == 0 || i + 8 <= a.count)) {
+            for (uint64_t k = i; k < a.count; ++k) {
+              float G;
+              if (kR32) {
+                G = reinterpret_cast<const float*>(a.dst)[k];
+                flag |= (uint32_t)!isfinite(G);
+              } else {
+                const uint32_t b = reinterpret_cast<const uint16_t*>(a.dst)[k];
+                flag |= D::nonfinite(b);
+                G = D::widen(b);
+              }
+              sq_acc(sumsq, __fmul_rn(G, inv));
+            }
+            continue;
+          }
+          float acc[8];
+          if (kR32) {
+            U8 w = ld256(reinterpret_cast<const float*>(a.dst) + i);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = __uint_as_float(w.x[j]);
+          } else {
+            U4 w = ld128(reinterpret_cast<const uint16_t*>(a.dst) + i);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = D::widen(h_get(w, j));
+          }
+          rs_emit8<DT, kR32>(a, i, acc, false, inv, sumsq, flag);
+        }
       }
     } else {
-      const uint64_t e = kVec ? (a.count < i + 8 ? a.count : i + 8) : i + 1;
-      for (uint64_t k = i; k < e; ++k) {
+      const uint64_t e = kVec ? (a.count < i0 + 8 ? a.count : i0 + 8) : i0 + 1;
+      for (uint64_t k = i0; k < e; ++k) {
         float acc;
         if (kReduce) {
           acc = D::widen(reinterpret_cast<const uint16_t*>(a.src[0])[k]);
-          for (int r = 1; r < a.n; ++r) acc = __fadd_rn(acc, D::widen(reinterpret_cast<const uint16_t*>(a.src[r])[k]));
+          for (int r = 1; r < n; ++r) acc = __fadd_rn(acc, D::widen(reinterpret_cast<const uint16_t*>(a.src[r])[k]));
         } else if (kR32) {
           acc = reinterpret_cast<const float*>(a.dst)[k];
         } else {
@@ -642,28 +704,41 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
           flag |= D::nonfinite(b);
           if (kReduce) reinterpret_cast<uint16_t*>(a.dst)[k] = (uint16_t)b;
         }
-        const float u = __fmul_rn(G, inv);
-        sq_acc(sumsq, u);
+        sq_acc(sumsq, __fmul_rn(G, inv));
       }
     }
   }
   grid_publish(sumsq, flag, a.part, a.slot, a.done_sig, a.wait_flags ? a.n : 0, a.epoch);
 }
 
+template <int DT, bool R32, bool RED, bool V>
+cudaError_t launch_rs_n(const RSArgs& a, int grid, cudaStream_t s) {
+  if constexpr (!V) {
+    k_reduce_scatter<DT, R32, RED, false, 0, 1><<<grid, kThreads, 0, s>>>(a);
+  } else if constexpr (!RED) {
+    k_reduce_scatter<DT, R32, RED, true, 0, 2><<<grid, kThreads, 0, s>>>(a);
+  } else {
+    switch (a.n) {
+      case 2: k_reduce_scatter<DT, R32, RED, true, 2, 4><<<grid, kThreads, 0, s>>>(a); break;
+      case 4: k_reduce_scatter<DT, R32, RED, true, 4, 2><<<grid, kThreads, 0, s>>>(a); break;
+      case 8: k_reduce_scatter<DT, R32, RED, true, 8, 1><<<grid, kThreads, 0, s>>>(a); break;
+      default: k_reduce_scatter<DT, R32, RED, true, 0, 1><<<grid, kThreads, 0, s>>>(a); break;
+    }
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s) {
   bool vec = aligned(a.dst, a.r32 ? 32 : 16);
   if (a.reduce)
     for (int r = 0; r < a.n; ++r) vec = vec && aligned(a.src[r], 16);
-#define ZR(DT, R32, RED, V) k_reduce_scatter<DT, R32, RED, V><<<grid, kThreads, 0, s>>>(a)
-#define ZRV(DT, R32, RED) do { if (vec) ZR(DT, R32, RED, true); else ZR(DT, R32, RED, false); } while (0)
+#define ZRV(DT, R32, RED) return vec ? launch_rs_n<DT, R32, RED, true>(a, grid, s) : launch_rs_n<DT, R32, RED, false>(a, grid, s)
 #define ZRR(DT, R32) do { if (a.reduce) ZRV(DT, R32, true); else ZRV(DT, R32, false); } while (0)
   if (a.dtype == DT_F16) { if (a.r32) ZRR(DT_F16, true); else ZRR(DT_F16, false); }
   else if (a.dtype == DT_BF16) { if (a.r32) ZRR(DT_BF16, true); else ZRR(DT_BF16, false); }
-  else return cudaErrorInvalidValue;
 #undef ZRR
 #undef ZRV
-#undef ZR
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;
 }
 
 // ---------------------------------------------------------------------------
