@@ -32,7 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "ZeRO step Gparams/s at 1/2/4/8 B200; % of HBM+NVLink roofline"
-NVLINK_GBS = 900.0   # per direction per GPU (nominal; task statement)
+NVLINK_GBS = 770.0   # per direction per GPU: the measured peer copy (B200_PROFILING.md); 900 nominal
 
 
 def parse():
@@ -410,6 +410,7 @@ def main():
                      "share_of_step": adam_ms / ms if adam_ms else None,
                      "note": None if adam_ms else "--graph: per-kernel events are not recorded inside the graph"},
         "step_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
+                          "hbm_gbs": hbm_peak, "nvlink_gbs": NVLINK_GBS if N > 1 else None,
                           "reduce_phase_ms": reduce_ms, "flatten_gbs": 4 * pp / (reduce_ms * 1e-3) / 1e9
                           if (N == 1 and reduce_ms) else None},
         "cuda_graph": bool(graph is not None),
@@ -432,6 +433,14 @@ def main():
         consumed = [torch.cuda.Event(), torch.cuda.Event()]
         rec = eng._info_host
         torch.cuda.synchronize()
+        # the PCIe bound of this leg: one pinned H2D of the step's gradients, alone
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(copy_stream):
+            h0.record(copy_stream)
+            bufs[1].copy_(host, non_blocking=True)
+            h1.record(copy_stream)
+        torch.cuda.synchronize()
+        h2d_ms = h0.elapsed_time(h1)
         barrier()
         K = args.e2e_steps
         t0 = time.perf_counter()
@@ -460,6 +469,9 @@ def main():
         line["e2e"] = {"value": psi_total / (e2e_ms * 1e-3) / 1e9, "unit": "Gparams/s",
                        "h2d_bytes_per_step": int(grad_buf.numel() * grad_buf.element_size()),
                        "d2h_bytes_per_step": 32, "ms_per_step": e2e_ms, "steps": K,
+                       "h2d_alone_ms": h2d_ms,
+                       "h2d_gbs": grad_buf.numel() * grad_buf.element_size() / (h2d_ms * 1e-3) / 1e9,
+                       "frac_of_h2d_bound": max(h2d_ms, ms) / e2e_ms,
                        "note": "host wall clock; H2D of step s+1 overlaps step s (double-buffered)"}
 
     if rank == 0 and not args.no_cpu_baseline:

@@ -207,7 +207,7 @@ struct zero_ctx {
   std::vector<AdamSeg> segs_host;
   bool segs_aligned8 = true;                       // every segment offset/count % 8 == 0
   int sms = 148;
-  int adam_variant = 11;                           // ZERO_ADAM_VARIANT (tuning; 11 = TMA 4096 x 2 stages)
+  int adam_variant = 21;                           // ZERO_ADAM_VARIANT (tuning; 21 = TMA in/out, 4096 x 2 stages)
   int flat_vecs = 4, flat_ctas = 4;                // ZERO_FLAT_VECS / ZERO_FLAT_CTAS
   int flat_tma = 0;                                // ZERO_FLAT_TMA: 0 off, else the TMA variant
 
@@ -847,7 +847,7 @@ zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads, cud
       if ((fp.dst_off | fp.count) & 7) tma_ok = false;
       if (fp.src && (reinterpret_cast<uintptr_t>(fp.src) & 15)) tma_ok = false;
     }
-    const int grid = grid_for((total + 2047) / 2048, tma_ok ? 1 : c->flat_ctas, c->sms);
+    const int grid = grid_for((total + 2047) / 2048, tma_ok ? flatten_tma_ctas_per_sm(c->flat_tma) : c->flat_ctas, c->sms);
     a.per_cta = align_up((total + grid - 1) / grid, 8);
     a.src_dtype = c->gdt;
     a.dst_dtype = c->pdt;

@@ -79,9 +79,22 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// A peer that never signals (a crashed rank, a protocol bug) must not wedge the GPU:
+// after kSpinTimeoutNs of waiting the kernel traps, which surfaces as a sticky CUDA
+// error in this process (ZERO_ECUDA) and leaves the device usable.
+constexpr uint64_t kSpinTimeoutNs = 300ull * 1000000000ull;
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void wait_all(const uint64_t* flags, int n, uint64_t epoch) {
+  const uint64_t t0 = globaltimer_ns();
   for (int j = 0; j < n; ++j)
-    while (ld_acquire_sys(flags + j) < epoch) __nanosleep(100);
+    while (ld_acquire_sys(flags + j) < epoch) {
+      __nanosleep(100);
+      if (globaltimer_ns() - t0 > kSpinTimeoutNs) __trap();
+    }
 }
 
 // TMA (cp.async.bulk) + mbarrier helpers
@@ -120,6 +133,24 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 }
 __device__ __forceinline__ void lds128(const void* p, uint32_t (&r)[4]) {
   asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(smem_u32(p)));
+}
+
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void sts128(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(p)), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ void lds64(const void* p, uint32_t& a, uint32_t& b) {
+  asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void sts64(void* p, uint32_t a, uint32_t b) {
+  asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(smem_u32(p)), "r"(a), "r"(b) : "memory");
 }
 
 // 8 16-bit values packed in a U4
@@ -533,6 +564,178 @@ cudaError_t launch_flatten_tma_t(const FlatArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// K2 (TMA in + TMA out): the producer thread streams each chunk of the bucket's
+// sources into shared memory with bulk loads and drains the finished chunk to the
+// bucket with a bulk store before refilling the stage.  For a same-dtype copy at
+// sigma = 1 the stage is stored as loaded and the consumers only read it (the N_d = 1
+// epilogue); otherwise they write the cast/scaled 16-bit chunk into an output slot.
+// Zero pieces (alignment gaps, padding) are zero-filled in shared memory.
+// Needs every piece offset/count % 8 == 0, 16-B aligned sources and destination.
+// ---------------------------------------------------------------------------
+template <int SDT, int DDT, bool kCopy, int T, int STAGES>
+__global__ void __launch_bounds__(T / 8 + 32) k_flatten_tma_st(const __grid_constant__ FlatArgs a) {
+  using S = SrcLoad<SDT>;
+  using D = H16<DDT>;
+  constexpr int kCons = T / 8;
+  constexpr uint32_t kInBytes = (uint32_t)T * S::kBytes;
+  constexpr uint32_t kStageBytes = kInBytes + (kCopy ? 0u : (uint32_t)T * 2u);
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  uint64_t* done = full + STAGES;
+  const uint64_t r0 = a.pieces[0].dst_off;
+  const uint64_t r1 = a.pieces[a.n_pieces - 1].dst_off + a.pieces[a.n_pieces - 1].count;
+  const uint64_t lo = r0 + (uint64_t)blockIdx.x * a.per_cta;
+  const uint64_t hi = lo + a.per_cta < r1 ? lo + a.per_cta : r1;
+  int p0 = 0;
+  while (p0 + 1 < a.n_pieces && a.pieces[p0 + 1].dst_off <= lo) ++p0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&done[i], kCons / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double sumsq = 0.0;
+  uint32_t flag = 0;
+  uint16_t* dst_base = reinterpret_cast<uint16_t*>(a.dst);
+  if (warp == kCons / 32) {  // ---- producer: loads ahead, stores behind
+    if (lane == 0 && lo < hi) {
+      const uint64_t pol = policy_evict_first();
+      uint64_t pend_start[STAGES];
+      uint32_t pend_n[STAGES];
+      auto drain = [&](uint32_t j) {
+        const int st = j % STAGES;
+        mbar_wait(&done[st], (j / STAGES) & 1);
+        bulk_s2g(dst_base + pend_start[st], smem + st * kStageBytes + (kCopy ? 0u : kInBytes), pend_n[st] * 2u, pol);
+        bulk_commit();
+      };
+      FlatCursor fc{lo, hi, p0};
+      uint64_t start;
+      uint32_t n;
+      int piece;
+      uint32_t it = 0;
+      for (; fc.next(a, T, start, n, piece); ++it) {
+        const int st = it % STAGES;
+        if (it >= (uint32_t)STAGES) {
+          drain(it - STAGES);
+          bulk_wait_read0();
+        }
+        pend_start[st] = start;
+        pend_n[st] = n;
+        const FlatPiece& pc = a.pieces[piece];
+        if (pc.src == nullptr) {
+          mbar_arrive(&full[st]);  // zero piece: the consumers fill the stage
+        } else {
+          mbar_expect_tx(&full[st], n * (uint32_t)S::kBytes);
+          bulk_g2s(smem + st * kStageBytes,
+                   reinterpret_cast<const char*>(pc.src) + (start - pc.dst_off) * S::kBytes, n * (uint32_t)S::kBytes,
+                   &full[st], pol);
+        }
+      }
+      for (uint32_t j = it > (uint32_t)STAGES ? it - STAGES : 0; j < it; ++j) drain(j);
+      bulk_wait_all0();
+    }
+  } else {  // ---- consumers
+    const float sigma = a.sigma;
+    const float inv = a.epilogue ? a.st->inv_cur : 0.0f;
+    FlatCursor fc{lo, hi, p0};
+    uint64_t start;
+    uint32_t n;
+    int piece;
+    for (uint32_t it = 0; fc.next(a, T, start, n, piece); ++it) {
+      const int st = it % STAGES;
+      mbar_wait(&full[st], (it / STAGES) & 1);
+      unsigned char* sb = smem + st * kStageBytes;
+      unsigned char* ob = sb + (kCopy ? 0u : kInBytes);
+      const uint32_t e = threadIdx.x * 8;
+      if (e < n) {
+        if (a.pieces[piece].src == nullptr) {
+          sts128(ob + e * 2, 0u, 0u, 0u, 0u);
+        } else if (kCopy) {
+          if (a.epilogue) {
+            uint32_t r[4];
+            lds128(sb + e * 2, r);
+            U4 g{{r[0], r[1], r[2], r[3]}};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t b = h_get(g, j);
+              flag |= D::nonfinite(b);
+              sq_acc(sumsq, __fmul_rn(D::widen(b), inv));
+            }
+          }
+        } else {
+          float x[8];
+          if (S::kBytes == 4) {
+            uint32_t r[4];
+            lds128(sb + e * 4, r);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) x[j] = __uint_as_float(r[j]);
+            lds128(sb + e * 4 + 16, r);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) x[4 + j] = __uint_as_float(r[j]);
+          } else {
+            uint32_t r[4];
+            lds128(sb + e * 2, r);
+            U4 g{{r[0], r[1], r[2], r[3]}};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = H16<SDT == DT_F32 ? DT_F16 : SDT>::widen(h_get(g, j));
+          }
+          U4 o;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t b = D::narrow(__fmul_rn(x[j], sigma));
+            h_set(o, j, b);
+            if (a.epilogue) {
+              flag |= D::nonfinite(b);
+              sq_acc(sumsq, __fmul_rn(D::widen(b), inv));
+            }
+          }
+          sts128(ob + e * 2, o.x[0], o.x[1], o.x[2], o.x[3]);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&done[st]);
+    }
+  }
+  if (a.epilogue) {
+    __syncthreads();
+    grid_publish(sumsq, flag, a.part, a.slot);
+  }
+}
+
+template <int SD, int DD, bool CP, int T, int STAGES>
+cudaError_t launch_flatten_tma_st_t(const FlatArgs& a, int grid, cudaStream_t s) {
+  const size_t smem = (size_t)STAGES * T * (SrcLoad<SD>::kBytes + (CP ? 0 : 2)) + 2 * STAGES * sizeof(uint64_t);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_flatten_tma_st<SD, DD, CP, T, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k_flatten_tma_st<SD, DD, CP, T, STAGES><<<grid, T / 8 + 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int T, int STAGES>
+cudaError_t launch_flatten_tma_st_ts(const FlatArgs& a, int grid, cudaStream_t s) {
+  const bool copy = (a.sigma == 1.0f) && (a.src_dtype == a.dst_dtype);
+#define ZT(SD, DD, CP) return launch_flatten_tma_st_t<SD, DD, CP, T, STAGES>(a, grid, s)
+  if (a.dst_dtype == DT_F16) {
+    if (a.src_dtype == DT_F16) { if (copy) ZT(DT_F16, DT_F16, true); else ZT(DT_F16, DT_F16, false); }
+    if (a.src_dtype == DT_F32) ZT(DT_F32, DT_F16, false);
+  } else if (a.dst_dtype == DT_BF16) {
+    if (a.src_dtype == DT_BF16) { if (copy) ZT(DT_BF16, DT_BF16, true); else ZT(DT_BF16, DT_BF16, false); }
+    if (a.src_dtype == DT_F32) ZT(DT_F32, DT_BF16, false);
+  }
+#undef ZT
+  return cudaErrorInvalidValue;
+}
+
 // TMA flatten (T 4096, 4 stages): measured 3.5 TB/s vs 4.2 TB/s for the register-staged
 // k_flatten on one stream (round-1 sweep), so it is off by default (ZERO_FLAT_TMA=1).
 template <int T, int STAGES>
@@ -552,7 +755,18 @@ cudaError_t launch_flatten_tma_ts(const FlatArgs& a, int grid, cudaStream_t s) {
 
 cudaError_t launch_flatten_tma(const FlatArgs& a, int grid, cudaStream_t s, int variant) {
   switch (variant) {
+    case 2: return launch_flatten_tma_st_ts<4096, 4>(a, grid, s);
+    case 3: return launch_flatten_tma_st_ts<4096, 2>(a, grid, s);
+    case 4: return launch_flatten_tma_st_ts<8192, 3>(a, grid, s);
+    case 5: return launch_flatten_tma_st_ts<2048, 4>(a, grid, s);
     default: return launch_flatten_tma_ts<4096, 4>(a, grid, s);
+  }
+}
+int flatten_tma_ctas_per_sm(int variant) {
+  switch (variant) {
+    case 3: return 2;
+    case 5: return 2;
+    default: return 1;
   }
 }
 
@@ -1142,6 +1356,167 @@ cudaError_t launch_adam_tma_t(const AdamArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// a5 (TMA in + TMA out): as k_adam_tma, but the consumers write the updated
+// p32/m/v back into the stage and the recast p16 into a per-stage slot, and the
+// producer thread drains the stage to global memory with 1-D bulk stores
+// (cp.async.bulk.global.shared::cta, SASS UBLKCP.G.S) before refilling it.
+// Consumer thread t handles elements [4t, 4t+4) and [4t + T/2, 4t + T/2 + 4) of
+// the tile: every shared-memory access of a warp is contiguous (no bank conflicts).
+// ---------------------------------------------------------------------------
+template <int PDT, int GDT, int T, int STAGES>
+__global__ void __launch_bounds__(T / 8 + 32, 1) k_adam_tma_st(const __grid_constant__ AdamArgs a) {
+  constexpr int kCons = T / 8;
+  using P = H16<PDT>;
+  constexpr int GB = (GDT == DT_F32) ? 4 : 2;
+  constexpr uint32_t kStageBytes = (uint32_t)T * (14 + GB);  // p32, m, v, G, p16
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  uint64_t* done = full + STAGES;
+  if (a.st->skip) return;  // overflow: skip the step (reading c-4)
+  const uint64_t lo = (uint64_t)blockIdx.x * a.per_cta;
+  if (lo >= a.total) return;
+  const uint64_t hi = lo + a.per_cta < a.total ? lo + a.per_cta : a.total;
+  int s0 = 0, s1 = a.n_segs - 1;
+  while (s0 < s1) {
+    const int mid = (s0 + s1 + 1) >> 1;
+    if (a.segs[mid].local_off <= lo) s0 = mid; else s1 = mid - 1;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&done[i], kCons / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kCons / 32) {  // ---- producer: loads ahead, stores behind
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      struct Pend { uint64_t start; uint32_t n; int64_t pd; };
+      Pend pend[STAGES];
+      auto drain = [&](uint32_t j) {  // tile j's results: stage -> global
+        const int st = j % STAGES;
+        mbar_wait(&done[st], (j / STAGES) & 1);
+        unsigned char* base = smem + st * kStageBytes;
+        const Pend& q = pend[st];
+        bulk_s2g(a.p32 + q.start, base, q.n * 4u, pol);
+        bulk_s2g(a.m + q.start, base + T * 4, q.n * 4u, pol);
+        bulk_s2g(a.v + q.start, base + T * 8, q.n * 4u, pol);
+        for (int d = 0; d < a.n_p16; ++d)
+          bulk_s2g(reinterpret_cast<uint16_t*>(a.p16[d]) + (q.start + q.pd), base + T * (12 + GB), q.n * 2u, pol);
+        bulk_commit();
+      };
+      TileCursor tc{lo, hi, s0};
+      uint64_t start;
+      uint32_t n;
+      int64_t gd, pd;
+      uint32_t it = 0;
+      for (; tc.next(a, T, start, n, gd, pd); ++it) {
+        const int st = it % STAGES;
+        if (it >= (uint32_t)STAGES) {
+          drain(it - STAGES);
+          bulk_wait_read0();  // the stage has been read out: it may be refilled
+        }
+        pend[st] = Pend{start, n, pd};
+        unsigned char* base = smem + st * kStageBytes;
+        mbar_expect_tx(&full[st], n * (12u + GB));
+        bulk_g2s(base, a.p32 + start, n * 4u, &full[st], pol);
+        bulk_g2s(base + T * 4, a.m + start, n * 4u, &full[st], pol);
+        bulk_g2s(base + T * 8, a.v + start, n * 4u, &full[st], pol);
+        bulk_g2s(base + T * 12, reinterpret_cast<const unsigned char*>(a.G) + (start + gd) * GB, n * (uint32_t)GB,
+                 &full[st], pol);
+      }
+      for (uint32_t j = it > (uint32_t)STAGES ? it - STAGES : 0; j < it; ++j) drain(j);
+      bulk_wait_all0();
+    }
+    return;
+  }
+
+  // ---- consumer warps
+  AdamScalars c;
+  c.inv = a.st->inv_adam;
+  c.step = a.st->step_f;
+  c.rsb2 = a.st->rsb2_f;
+  c.clip = a.st->clip_f;
+  c.beta1 = a.beta1;
+  c.beta2 = a.beta2;
+  c.eps = a.eps;
+  c.omb1 = a.omb1;
+  c.omb2 = a.omb2;
+  c.lrwd = a.lrwd;
+  c.wd = a.wd;
+  TileCursor tc{lo, hi, s0};
+  uint64_t start;
+  uint32_t n;
+  int64_t gd, pd;
+  for (uint32_t it = 0; tc.next(a, T, start, n, gd, pd); ++it) {
+    const int st = it % STAGES;
+    mbar_wait(&full[st], (it / STAGES) & 1);
+    unsigned char* base = smem + st * kStageBytes;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t e = threadIdx.x * 4 + h * (T / 2);
+      if (e < n) {  // n % 8 == 0 and e % 4 == 0: all 4 elements are in the tile
+        uint32_t p[4], m[4], v[4];
+        float G[4];
+        lds128(base + e * 4, p);
+        lds128(base + T * 4 + e * 4, m);
+        lds128(base + T * 8 + e * 4, v);
+        if (GB == 4) {
+          uint32_t r[4];
+          lds128(base + T * 12 + e * 4, r);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) G[j] = __uint_as_float(r[j]);
+        } else {
+          uint32_t r0, r1;
+          lds64(base + T * 12 + e * 2, r0, r1);
+          constexpr int GD16 = GDT == DT_F32 ? DT_F16 : GDT;
+          G[0] = H16<GD16>::widen(r0 & 0xFFFFu);
+          G[1] = H16<GD16>::widen(r0 >> 16);
+          G[2] = H16<GD16>::widen(r1 & 0xFFFFu);
+          G[3] = H16<GD16>::widen(r1 >> 16);
+        }
+        uint32_t o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float pj = __uint_as_float(p[j]), mj = __uint_as_float(m[j]), vj = __uint_as_float(v[j]);
+          adam_elem(pj, mj, vj, G[j], c);
+          p[j] = __float_as_uint(pj);
+          m[j] = __float_as_uint(mj);
+          v[j] = __float_as_uint(vj);
+          o[j] = P::narrow(pj);
+        }
+        sts128(base + e * 4, p[0], p[1], p[2], p[3]);
+        sts128(base + T * 4 + e * 4, m[0], m[1], m[2], m[3]);
+        sts128(base + T * 8 + e * 4, v[0], v[1], v[2], v[3]);
+        sts64(base + T * (12 + GB) + e * 2, o[0] | (o[1] << 16), o[2] | (o[3] << 16));
+      }
+    }
+    // make this warp's generic-proxy writes of the stage visible to the bulk stores
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&done[st]);
+  }
+}
+
+template <int PD, int GD, int T, int STAGES>
+cudaError_t launch_adam_tma_st_t(const AdamArgs& a, int grid, cudaStream_t s) {
+  constexpr int GB = (GD == DT_F32) ? 4 : 2;
+  const size_t smem = (size_t)STAGES * T * (14 + GB) + 2 * STAGES * sizeof(uint64_t);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_adam_tma_st<PD, GD, T, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k_adam_tma_st<PD, GD, T, STAGES><<<grid, T / 8 + 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 // Variants kept from the round-1 sweep (GPT-2 1.5B step on 1x B200, % of the measured
 // 6456.8 GB/s copy peak; profiles/r01_summary.md):
 //   0 = register-staged, 2 CTAs/SM (85.5 %)     1 = register-staged, 4 CTAs/SM, <= 64 regs (90.1 %)
@@ -1155,10 +1530,11 @@ int adam_ctas_per_sm(int variant) {
     case 5: return 1;
     case 11: return 1;
     case 16: return 2;
+    case 21: case 22: case 23: case 24: case 25: case 26: case 27: return 1;
     default: return 2;
   }
 }
-bool adam_variant_is_tma(int variant) { return variant == 5 || variant == 11 || variant == 16; }
+bool adam_variant_is_tma(int variant) { return variant == 5 || variant == 11 || variant == 16 || (variant >= 21 && variant <= 27); }
 
 template <int PD, int GD>
 cudaError_t launch_adam_t(const AdamArgs& a, int grid, cudaStream_t s, int variant) {
@@ -1166,6 +1542,13 @@ cudaError_t launch_adam_t(const AdamArgs& a, int grid, cudaStream_t s, int varia
     case 5: return launch_adam_tma_t<PD, GD, 2048, 4>(a, grid, s);
     case 11: return launch_adam_tma_t<PD, GD, 4096, 2>(a, grid, s);
     case 16: return launch_adam_tma_t<PD, GD, 2048, 2>(a, grid, s);
+    case 21: return launch_adam_tma_st_t<PD, GD, 4096, 2>(a, grid, s);
+    case 22: return launch_adam_tma_st_t<PD, GD, 4096, 3>(a, grid, s);
+    case 23: return launch_adam_tma_st_t<PD, GD, 2048, 4>(a, grid, s);
+    case 24: return launch_adam_tma_st_t<PD, GD, 2048, 3>(a, grid, s);
+    case 25: return launch_adam_tma_st_t<PD, GD, 6144, 2>(a, grid, s);
+    case 26: return launch_adam_tma_st_t<PD, GD, 3072, 2>(a, grid, s);
+    case 27: return launch_adam_tma_st_t<PD, GD, 3072, 3>(a, grid, s);
     case 1: k_adam<PD, GD, 4, 1><<<grid, kThreads, 0, s>>>(a); break;
     default: k_adam<PD, GD, 2, 1><<<grid, kThreads, 0, s>>>(a); break;
   }

@@ -151,6 +151,7 @@ struct ShardIOArgs {           // checkpoint: per-tensor fp32 piece <-> owned sh
 // launchers (kernels.cu); return the launch error
 cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s, int vecs);
 cudaError_t launch_flatten_tma(const FlatArgs& a, int grid, cudaStream_t s, int variant);
+int flatten_tma_ctas_per_sm(int variant);
 cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_decide_local(const Slot* slots, int n_slots, RankPartial* out, cudaStream_t s);
 struct PartialPtrs {
