@@ -738,6 +738,9 @@ cudaError_t launch_flatten_tma_st_ts(const FlatArgs& a, int grid, cudaStream_t s
 
 // TMA flatten (T 4096, 4 stages): measured 3.5 TB/s vs 4.2 TB/s for the register-staged
 // k_flatten on one stream (round-1 sweep), so it is off by default (ZERO_FLAT_TMA=1).
+// TMA in + TMA out (ZERO_FLAT_TMA=2): the reduce phase of the 1.5B step takes 1.38 ms vs
+// 1.09 ms for k_flatten on three streams (4096x2 on 2 CTAs/SM 1.46 ms, 2048x4 on 2 CTAs/SM
+// 1.44 ms), so it is off as well.
 template <int T, int STAGES>
 cudaError_t launch_flatten_tma_ts(const FlatArgs& a, int grid, cudaStream_t s) {
   const bool copy = (a.sigma == 1.0f) && (a.src_dtype == a.dst_dtype);
@@ -756,19 +759,10 @@ cudaError_t launch_flatten_tma_ts(const FlatArgs& a, int grid, cudaStream_t s) {
 cudaError_t launch_flatten_tma(const FlatArgs& a, int grid, cudaStream_t s, int variant) {
   switch (variant) {
     case 2: return launch_flatten_tma_st_ts<4096, 4>(a, grid, s);
-    case 3: return launch_flatten_tma_st_ts<4096, 2>(a, grid, s);
-    case 4: return launch_flatten_tma_st_ts<8192, 3>(a, grid, s);
-    case 5: return launch_flatten_tma_st_ts<2048, 4>(a, grid, s);
     default: return launch_flatten_tma_ts<4096, 4>(a, grid, s);
   }
 }
-int flatten_tma_ctas_per_sm(int variant) {
-  switch (variant) {
-    case 3: return 2;
-    case 5: return 2;
-    default: return 1;
-  }
-}
+int flatten_tma_ctas_per_sm(int) { return 1; }
 
 // ---------------------------------------------------------------------------
 // a2+a3: pull reduce-scatter of one bucket slice over a peer table (fp32 sum in
@@ -1517,38 +1511,29 @@ cudaError_t launch_adam_tma_st_t(const AdamArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// Variants kept from the round-1 sweep (GPT-2 1.5B step on 1x B200, % of the measured
-// 6456.8 GB/s copy peak; profiles/r01_summary.md):
+// Variants kept from the round-1 sweeps (GPT-2 1.5B step on 1x B200, % of the measured
+// copy peak of the box; profiles/r01_summary.md):
 //   0 = register-staged, 2 CTAs/SM (85.5 %)     1 = register-staged, 4 CTAs/SM, <= 64 regs (90.1 %)
-//   5 = TMA, T 2048 x 4 stages, 1 CTA/SM (92.6 %)   16 = TMA, 2048 x 2, 2 CTAs/SM (93.5 %)
-//  11 = TMA, T 4096 x 2 stages, 1 CTA/SM: 512 consumers + 1 producer warp (97.1-97.4 %, default)
-// (also measured and dropped: 1024x{4,6} 61-89 %, 2048x{3,6} 86-91 %, 4096x3 92 %, 6144x2 93 %,
-//  3072x2 92 %, 4096x1 70 %, register unroll-2 / 3 CTAs 81 %, 1 CTA unroll-4 87 %)
+//  11 = TMA loads, STG stores, T 4096 x 2 stages, 1 CTA/SM: 512 consumers + 1 producer warp (96.1 %)
+//  21 = TMA loads and TMA stores (k_adam_tma_st), T 4096 x 2 stages, 1 CTA/SM (99.3 %, default)
+// (also measured and dropped -- TMA loads + STG: 2048x4 92.6 %, 2048x2 on 2 CTAs/SM 93.5 %,
+//  1024x{4,6} 61-89 %, 2048x{3,6} 86-91 %, 4096x3 92 %, 6144x2 93 %, 3072x2 92 %, 4096x1 70 %;
+//  TMA loads + TMA stores: 4096x3 94.9 %, 2048x4 95.2 %, 2048x3 98.3 %, 6144x2 95.5 %,
+//  3072x2 94.9 %, 3072x3 95.5 %; register unroll-2 / 3 CTAs 81 %, 1 CTA unroll-4 87 %)
 int adam_ctas_per_sm(int variant) {
   switch (variant) {
     case 1: return 4;
-    case 5: return 1;
-    case 11: return 1;
-    case 16: return 2;
-    case 21: case 22: case 23: case 24: case 25: case 26: case 27: return 1;
+    case 11: case 21: return 1;
     default: return 2;
   }
 }
-bool adam_variant_is_tma(int variant) { return variant == 5 || variant == 11 || variant == 16 || (variant >= 21 && variant <= 27); }
+bool adam_variant_is_tma(int variant) { return variant == 11 || variant == 21; }
 
 template <int PD, int GD>
 cudaError_t launch_adam_t(const AdamArgs& a, int grid, cudaStream_t s, int variant) {
   switch (variant) {
-    case 5: return launch_adam_tma_t<PD, GD, 2048, 4>(a, grid, s);
     case 11: return launch_adam_tma_t<PD, GD, 4096, 2>(a, grid, s);
-    case 16: return launch_adam_tma_t<PD, GD, 2048, 2>(a, grid, s);
     case 21: return launch_adam_tma_st_t<PD, GD, 4096, 2>(a, grid, s);
-    case 22: return launch_adam_tma_st_t<PD, GD, 4096, 3>(a, grid, s);
-    case 23: return launch_adam_tma_st_t<PD, GD, 2048, 4>(a, grid, s);
-    case 24: return launch_adam_tma_st_t<PD, GD, 2048, 3>(a, grid, s);
-    case 25: return launch_adam_tma_st_t<PD, GD, 6144, 2>(a, grid, s);
-    case 26: return launch_adam_tma_st_t<PD, GD, 3072, 2>(a, grid, s);
-    case 27: return launch_adam_tma_st_t<PD, GD, 3072, 3>(a, grid, s);
     case 1: k_adam<PD, GD, 4, 1><<<grid, kThreads, 0, s>>>(a); break;
     default: k_adam<PD, GD, 2, 1><<<grid, kThreads, 0, s>>>(a); break;
   }

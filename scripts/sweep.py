@@ -7,7 +7,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 import argparse
 ap = argparse.ArgumentParser()
-ap.add_argument("--adam", default="0,1,5,11,16")
+ap.add_argument("--adam", default="0,1,11,21")
 ap.add_argument("--flat", default="")          # e.g. "4x4,4x8"  (vecs x ctas)
 ap.add_argument("--base", default="")          # fixed env for every run, e.g. "ZERO_ADAM_VARIANT=1"
 ap.add_argument("--flat-tma", default="")      # e.g. "1,2,3,4"
