@@ -13,6 +13,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "zero_internal.h"
@@ -151,6 +152,18 @@ __device__ __forceinline__ void lds64(const void* p, uint32_t& a, uint32_t& b) {
 }
 __device__ __forceinline__ void sts64(void* p, uint32_t a, uint32_t b) {
   asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(smem_u32(p)), "r"(a), "r"(b) : "memory");
+}
+
+// opt a kernel in to > 48 KB of dynamic shared memory, once per device
+template <typename Kernel>
+cudaError_t allow_dynamic_smem(Kernel k, size_t smem, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  if (cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) return e;
+  done.fetch_or(bit, std::memory_order_release);
+  return cudaSuccess;
 }
 
 // 8 16-bit values packed in a U4
@@ -553,13 +566,8 @@ __global__ void __launch_bounds__(T / 8 + 32, 1) k_flatten_tma(const __grid_cons
 template <int SD, int DD, bool CP, int T, int STAGES>
 cudaError_t launch_flatten_tma_t(const FlatArgs& a, int grid, cudaStream_t s) {
   const size_t smem = (size_t)STAGES * T * SrcLoad<SD>::kBytes + 2 * STAGES * sizeof(uint64_t);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_flatten_tma<SD, DD, CP, T, STAGES>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};  // one bit per device
+  if (cudaError_t e = allow_dynamic_smem(k_flatten_tma<SD, DD, CP, T, STAGES>, smem, configured)) return e;
   k_flatten_tma<SD, DD, CP, T, STAGES><<<grid, T / 8 + 32, smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -710,13 +718,8 @@ __global__ void __launch_bounds__(T / 8 + 32) k_flatten_tma_st(const __grid_cons
 template <int SD, int DD, bool CP, int T, int STAGES>
 cudaError_t launch_flatten_tma_st_t(const FlatArgs& a, int grid, cudaStream_t s) {
   const size_t smem = (size_t)STAGES * T * (SrcLoad<SD>::kBytes + (CP ? 0 : 2)) + 2 * STAGES * sizeof(uint64_t);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_flatten_tma_st<SD, DD, CP, T, STAGES>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};  // one bit per device
+  if (cudaError_t e = allow_dynamic_smem(k_flatten_tma_st<SD, DD, CP, T, STAGES>, smem, configured)) return e;
   k_flatten_tma_st<SD, DD, CP, T, STAGES><<<grid, T / 8 + 32, smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -1339,13 +1342,8 @@ template <int PD, int GD, int T, int STAGES>
 cudaError_t launch_adam_tma_t(const AdamArgs& a, int grid, cudaStream_t s) {
   constexpr int GB = (GD == DT_F32) ? 4 : 2;
   const size_t smem = (size_t)STAGES * T * (12 + GB) + 2 * STAGES * sizeof(uint64_t);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_adam_tma<PD, GD, T, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};  // one bit per device
+  if (cudaError_t e = allow_dynamic_smem(k_adam_tma<PD, GD, T, STAGES>, smem, configured)) return e;
   k_adam_tma<PD, GD, T, STAGES><<<grid, T / 8 + 32, smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -1500,13 +1498,8 @@ template <int PD, int GD, int T, int STAGES>
 cudaError_t launch_adam_tma_st_t(const AdamArgs& a, int grid, cudaStream_t s) {
   constexpr int GB = (GD == DT_F32) ? 4 : 2;
   const size_t smem = (size_t)STAGES * T * (14 + GB) + 2 * STAGES * sizeof(uint64_t);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_adam_tma_st<PD, GD, T, STAGES>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};  // one bit per device
+  if (cudaError_t e = allow_dynamic_smem(k_adam_tma_st<PD, GD, T, STAGES>, smem, configured)) return e;
   k_adam_tma_st<PD, GD, T, STAGES><<<grid, T / 8 + 32, smem, s>>>(a);
   return cudaGetLastError();
 }
