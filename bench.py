@@ -54,6 +54,7 @@ def parse():
                     help="capture one whole step (all zero_reduce_grads + zero_step) in a CUDA graph and time replays")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-parallel", action="store_true", help="skip the all-cores oracle baseline")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     return ap.parse_args()
 
@@ -181,6 +182,52 @@ def oracle_sample_run(tensors, dtype: str, seed: int, steps: int, warmup: int, b
     desc = (f"first {n} params of the layout in forward order ({len(sample)} tensors), N_d=1, "
             f"{steps} oracle steps (numpy fp32, 1 thread), inputs pre-generated")
     return n * steps / dt / 1e9, desc, n, dt
+
+
+def _oracle_worker(args):
+    tensors, dtype, seed, n_cap, budget_s, barrier = args
+    import torch
+    torch.set_num_threads(1)
+    import synth
+    from oracle import step as OS
+    cfg = OS.AdamConfig.defaults(dtype, grad_dtype=dtype)
+    sample, n = [], 0
+    for t in tensors:
+        if n >= n_cap:
+            break
+        take = min(t.numel, n_cap - n)
+        sample.append(synth.TensorSpec(t.name, take, 0, t.role))
+        n += take
+    st = OS.init_state(synth.master_values(sample, seed), cfg)
+    grads = [[OS.grads_from_torch(synth.grads16(sample, seed, 0, s, dtype))] for s in range(2)]
+    OS.step(st, grads[0], cfg)                   # warm-up
+    barrier.wait()
+    t0, steps = time.perf_counter(), 0
+    while True:
+        OS.step(st, grads[steps % 2], cfg)
+        steps += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    return n * steps, time.perf_counter() - t0
+
+
+def oracle_parallel_run(tensors, dtype: str, seed: int, budget_s: float, procs: int):
+    """The same oracle, unchanged, in `procs` forked worker processes (one per host core),
+    each stepping its own copy of a prefix sample for ~budget_s.  Elementwise work is
+    independent per element, so the aggregate rate is what the oracle reaches on all
+    cores.  Returns (Gparams/s, description)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    n_cap = 1 << 23
+    with ctx.Manager() as man:
+        barrier = man.Barrier(procs)
+        with ctx.Pool(procs) as pool:
+            res = pool.map(_oracle_worker, [(tensors, dtype, seed + w, n_cap, budget_s, barrier) for w in range(procs)])
+    work = sum(r[0] for r in res)
+    dt = max(r[1] for r in res)
+    desc = (f"{procs} worker processes (1 thread each), each stepping its own copy of the first {n_cap} params "
+            f"of the layout for ~{budget_s:.0f} s (numpy fp32 oracle, unchanged); aggregate = total params x steps / slowest worker")
+    return work / dt / 1e9, desc
 
 
 def run_reference(args, tensors, psi_total):
@@ -379,18 +426,20 @@ def main():
     pp = info.psi_padded
     # step roofline: sum over phases of max(HBM bytes / BW_HBM, NVLink bytes / BW_NVL)
     N = world
-    hbm = hbm_peak * 1e9
-    t_flat = 4 * pp / hbm
-    if N == 1:
-        t_roof = t_flat + 28 * pp / hbm
-    else:
+
+    def t_roof_at(hbm_gbs):
+        hbm = hbm_gbs * 1e9
+        t_flat = 4 * pp / hbm
+        if N == 1:
+            return t_flat + 28 * pp / hbm
         nvl = 2 * pp * (N - 1) / N / (NVLINK_GBS * 1e9)      # one RS or one AG of Psi' 16-bit elements
         if args.stage == 3:                                   # [AG fwd] -> [flatten + RS + AG bwd] -> [Adam]
-            t_roof = max(2 * pp / hbm, nvl) + max((4 * pp + 2 * pp + 2 * pp / N) / hbm, 2 * nvl) + 28 * pp / N / hbm
-        else:                                                 # [flatten] -> [RS] -> [Adam || AG]
-            t_rs = max((2 * pp + 2 * pp / N) / hbm, nvl)
-            t_adam_ag = max((28 * pp / N + 2 * pp) / hbm, nvl)
-            t_roof = t_flat + t_rs + t_adam_ag
+            return max(2 * pp / hbm, nvl) + max((4 * pp + 2 * pp + 2 * pp / N) / hbm, 2 * nvl) + 28 * pp / N / hbm
+        t_rs = max((2 * pp + 2 * pp / N) / hbm, nvl)
+        if args.stage == 0:                                   # [flatten] -> [RS] -> [AG of the sums] -> [full Adam]
+            return t_flat + t_rs + max(2 * pp / hbm, nvl) + 28 * pp / hbm
+        return t_flat + t_rs + max((28 * pp / N + 2 * pp) / hbm, nvl)   # [flatten] -> [RS] -> [Adam || AG]
+    t_roof = t_roof_at(hbm_peak)
     line = {
         "metric": METRIC, "value": value, "unit": "Gparams/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms,
@@ -410,6 +459,8 @@ def main():
                      "share_of_step": adam_ms / ms if adam_ms else None,
                      "note": None if adam_ms else "--graph: per-kernel events are not recorded inside the graph"},
         "step_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
+                          "hbm_gbs": hbm_peak, "nvlink_gbs": NVLINK_GBS if N > 1 else None,
+                          "frac_at_spec_hbm_8tbs": t_roof_at(8000.0) * 1e3 / ms,
                           "hbm_gbs": hbm_peak, "nvlink_gbs": NVLINK_GBS if N > 1 else None,
                           "reduce_phase_ms": reduce_ms, "flatten_gbs": 4 * pp / (reduce_ms * 1e-3) / 1e9
                           if (N == 1 and reduce_ms) else None},
@@ -477,6 +528,14 @@ def main():
     if rank == 0 and not args.no_cpu_baseline:
         v, desc, n, dt = oracle_sample_run(tensors, args.dtype, args.seed, 2, 0, args.cpu_budget_s)
         line["cpu_baseline"] = {"value": v, "unit": "Gparams/s", "cores": 1, "kind": "oracle", "sample": desc}
+        procs = len(os.sched_getaffinity(0))
+        if procs > 1 and not args.no_cpu_parallel:
+            try:
+                pv, pdesc = oracle_parallel_run(tensors, args.dtype, args.seed, min(args.cpu_budget_s, 10.0), procs)
+                line["cpu_baseline_all_cores"] = {"value": pv, "unit": "Gparams/s", "cores": procs, "kind": "oracle",
+                                                  "sample": pdesc}
+            except Exception as exc:  # a host without fork/shared-memory support
+                line["cpu_baseline_all_cores"] = {"value": None, "note": f"not measured: {exc}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
