@@ -353,6 +353,75 @@ const char* zero_last_error(const struct zero_ctx* ctx);
  * Destroying one member of a simulated group dissolves the group. */
 void zero_destroy(struct zero_ctx* ctx);
 
+/* ---------------------------------------------------------------------------
+ * P_a / P_a+cpu: partitioned activation checkpoints over a model-parallel group
+ * (ZeRO-R, §6.1; communication P:486-498 §8).  Under tensor-slicing MP
+ * every MP rank holds a replicated copy of each layer's input activation; P_a keeps
+ * only this rank's 1/N_m slice of the checkpoint after the layer's forward and
+ * re-materializes the replicated copy with an all-gather right before the
+ * recompute in backward.  P_a+cpu keeps the slice in pinned host memory
+ * and brings it back before the gather (2x the slice over PCIe).
+ * The gather is, element for element, the saved activation (oracle/activation.py).
+ *
+ * Partition (reading R-Pa1): one checkpoint has `numel` 16-bit elements, padded to
+ * `padded` = a multiple of N_m * 8; rank r keeps [r*slice, (r+1)*slice), slice =
+ * padded / N_m (16-byte granules).
+ * Transports: LOCAL (n_m == 1), PEER (zero_pa_sim_group: N_m contexts on one device;
+ * the gather pulls every peer's slice with 128-bit loads) and NCCL (one process per
+ * GPU: in-place ncclAllGather into a staging buffer, then a copy out).
+ * Arenas (zero_pa_info): device = n_layers * slice * 2 B (P_a) or one slice staging
+ * slot (P_a+cpu, PEER) or + `padded` staging elements (NCCL); host = n_layers * slice
+ * * 2 B of pinned memory (P_a+cpu only; caller-allocated, e.g. torch pin_memory).
+ * All calls are stream-ordered on the context's stream; errors as for zero_ctx
+ * (ZERO_EINVAL bad argument, ZERO_ESTATE call order, ZERO_ECUDA/ENCCL sticky).
+ * ------------------------------------------------------------------------- */
+struct zero_pa_ctx;
+typedef struct {
+  uint64_t numel, padded, slice;          /* elements per checkpoint / padded / per rank */
+  uint64_t device_bytes, host_bytes;      /* arenas the caller allocates */
+  uint32_t n_layers, n_m, rank, offload;
+} zero_pa_info;
+typedef struct {                          /* cumulative counters */
+  uint64_t saved_elems;                   /* elements this rank kept (its slices) */
+  uint64_t gathered_elems;                /* elements received from other MP ranks */
+  uint64_t d2h_bytes, h2d_bytes;          /* P_a+cpu PCIe traffic */
+} zero_pa_counters;
+
+/* numel: elements of one checkpoint (b*s*h); n_layers checkpoints (one per layer).
+ * dtype FP16 | BF16.  offload: 0 = P_a, 1 = P_a+cpu.  transport/nccl_comm/stream as
+ * for zero_init.  Errors: ZERO_EINVAL (n_m outside 1..ZERO_MAX_RANKS, rank >= n_m,
+ * numel == 0, n_layers == 0, dtype, LOCAL with n_m > 1, NCCL without a comm). */
+zero_status zero_pa_init(int n_m, int rank, uint32_t n_layers, uint64_t numel, zero_dtype dtype, int offload,
+                         zero_transport transport, void* nccl_comm, void* stream, struct zero_pa_ctx** out);
+zero_status zero_pa_get_info(const struct zero_pa_ctx* ctx, zero_pa_info* out);
+/* Bind the caller's arenas (device: >= 256-B aligned, device_bytes; host: pinned,
+ * host_bytes, NULL when 0).  The library never frees them. */
+zero_status zero_pa_bind(struct zero_pa_ctx* ctx, void* device_arena, void* host_arena);
+/* Link n PEER contexts of one process and device (rank r at index r, same numel,
+ * n_layers, dtype, offload, stream, all bound) into an MP group. */
+zero_status zero_pa_sim_group(struct zero_pa_ctx* const* ranks, int n);
+/* After layer `layer`'s forward: keep this rank's slice of the checkpoint `act`
+ * (device pointer, numel elements; borrowed until the stream work completes) in the
+ * device store, or copy it to the host store (P_a+cpu).  Re-saving a layer
+ * overwrites it. */
+zero_status zero_pa_save(struct zero_pa_ctx* ctx, uint32_t layer, const void* act);
+/* P_a+cpu: bring this rank's slice of `layer` back into the device staging slot
+ * (H2D), ahead of the gather; every rank of the group must prefetch a layer before
+ * any rank gathers it.  P_a: no-op.  ZERO_ESTATE if the layer was never saved. */
+zero_status zero_pa_prefetch(struct zero_pa_ctx* ctx, uint32_t layer);
+/* Before the recompute: write the replicated checkpoint of `layer` (numel elements)
+ * into act_out (device).  ZERO_ESTATE if some rank of the group has not saved (P_a)
+ * or prefetched (P_a+cpu) the layer. */
+zero_status zero_pa_gather(struct zero_pa_ctx* ctx, uint32_t layer, void* act_out);
+zero_status zero_pa_get_counters(const struct zero_pa_ctx* ctx, zero_pa_counters* out);
+const char* zero_pa_last_error(const struct zero_pa_ctx* ctx);
+/* Synchronize the stream and free the context (not the arenas); dissolves its group. */
+void zero_pa_destroy(struct zero_pa_ctx* ctx);
+/* P:419 closed form: per-GPU bytes of one checkpointed b x s x h activation per layer,
+ * divided by the MP degree (P_a) -- floor(layers*batch*seq*hidden*elem_bytes / n_m). */
+uint64_t zero_pa_checkpoint_bytes(uint64_t layers, uint64_t batch, uint64_t seq, uint64_t hidden, int n_m,
+                                  int elem_bytes);
+
 /* Pure host functions (no GPU): the closed forms the runtime reports against. */
 /* Fig. 1 / Table 1: per-device model-state bytes for stage 0..3 (floor). */
 uint64_t zero_model_state_bytes(uint64_t psi, int K, int n_d, int stage);

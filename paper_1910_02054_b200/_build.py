@@ -49,7 +49,7 @@ def _stale(out: str, srcs) -> bool:
 def build(force: bool = False, verbose: bool = False) -> list:
     built = []
     nccl = nccl_root()
-    srcs = [os.path.join(CSRC, "kernels.cu"), os.path.join(CSRC, "engine.cpp")]
+    srcs = [os.path.join(CSRC, "kernels.cu"), os.path.join(CSRC, "engine.cpp"), os.path.join(CSRC, "activation.cu")]
     deps = srcs + [os.path.join(CSRC, "zero_internal.h"), os.path.join(ROOT, "include", "zero_b200.h")]
     if force or _stale(LIB, deps):
         cmd = [_nvcc()] + COMMON + ["-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include"),

@@ -101,7 +101,10 @@ EXPORTS = ["zero_plan_layout", "zero_init", "zero_buffer_sizes", "zero_bind_buff
            "zero_peer_export", "zero_peer_open", "zero_export_state", "zero_import_state",
            "zero_load_master", "zero_set_grad_ptrs", "zero_reduce_grads", "zero_step", "zero_gather_params",
            "zero_release_params", "zero_param_view", "zero_query", "zero_last_error", "zero_destroy",
-           "zero_model_state_bytes", "zero_comm_elems_per_rank", "zero_abi_version"]
+           "zero_model_state_bytes", "zero_comm_elems_per_rank", "zero_abi_version",
+           "zero_pa_init", "zero_pa_get_info", "zero_pa_bind", "zero_pa_sim_group", "zero_pa_save",
+           "zero_pa_prefetch", "zero_pa_gather", "zero_pa_get_counters", "zero_pa_last_error", "zero_pa_destroy",
+           "zero_pa_checkpoint_bytes"]
 
 
 def _load():
@@ -135,6 +138,19 @@ def _load():
         "zero_model_state_bytes": ([C.c_uint64, C.c_int, C.c_int, C.c_int], C.c_uint64),
         "zero_comm_elems_per_rank": ([C.c_uint64, C.c_int, C.c_int], C.c_uint64),
         "zero_abi_version": ([], C.c_int),
+        # P_a / P_a+cpu (include/zero_b200.h; binding classes in activation.py)
+        "zero_pa_init": ([C.c_int, C.c_int, C.c_uint32, C.c_uint64, C.c_int, C.c_int, C.c_int, P, P, C.POINTER(P)],
+                         C.c_int),
+        "zero_pa_get_info": ([P, P], C.c_int),
+        "zero_pa_bind": ([P, P, P], C.c_int),
+        "zero_pa_sim_group": ([C.POINTER(P), C.c_int], C.c_int),
+        "zero_pa_save": ([P, C.c_uint32, P], C.c_int),
+        "zero_pa_prefetch": ([P, C.c_uint32], C.c_int),
+        "zero_pa_gather": ([P, C.c_uint32, P], C.c_int),
+        "zero_pa_get_counters": ([P, P], C.c_int),
+        "zero_pa_last_error": ([P], C.c_char_p),
+        "zero_pa_destroy": ([P], None),
+        "zero_pa_checkpoint_bytes": ([C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.c_int], C.c_uint64),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
