@@ -238,6 +238,7 @@ struct zero_ctx {
   std::vector<void*> ipc_mapped;                   // bases to cudaIpcCloseMemHandle
   std::vector<std::pair<int, uint64_t>> pool_last; // per pool slot: (bucket, epoch) of its last use
   size_t off_sig_flat = 0, off_sig_rs = 0, off_sig_part = 0, off_sig_adam = 0, off_gathered = 0;
+  size_t off_sig_hello = 0, off_hello_result = 0;
   uint64_t epoch() const { return counters.steps + 1; }
   uint64_t* sig(int r, size_t off, size_t idx) const {  // signal slot in rank r's scratch
     return reinterpret_cast<uint64_t*>(peer_scratch[r] + off) + idx;
@@ -339,7 +340,7 @@ int grid_for(uint64_t work_items, int per_sm, int sms) {
 // bytes of the scratch arena and the offsets inside it
 struct ScratchLayout {
   size_t st, slots, part_compute, part_flat2, part_flat3, part_flat4, part_comm, my_partial, gathered, segs, sig_flat, sig_rs, sig_part, sig_adam,
-      total;
+      sig_hello, hello_result, total;
 };
 // sig_flat[k][r] / sig_rs[k][r]: epoch at which rank r flattened / finished reducing bucket k
 // sig_part[r] / sig_adam[r]: epoch at which rank r published its partial / finished Adam
@@ -361,6 +362,8 @@ ScratchLayout scratch_layout(int n_slots, size_t n_segs, size_t n_buckets) {
   s.sig_rs = take(sizeof(uint64_t) * ZERO_MAX_RANKS * std::max<size_t>(n_buckets, 1));
   s.sig_part = take(sizeof(uint64_t) * ZERO_MAX_RANKS);
   s.sig_adam = take(sizeof(uint64_t) * ZERO_MAX_RANKS);
+  s.sig_hello = take(sizeof(uint64_t) * ZERO_MAX_RANKS);   // zero_peer_open's handshake
+  s.hello_result = take(sizeof(uint32_t));
   s.total = o;
   return s;
 }
@@ -610,6 +613,8 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   c->off_sig_rs = sl.sig_rs;
   c->off_sig_part = sl.sig_part;
   c->off_sig_adam = sl.sig_adam;
+  c->off_sig_hello = sl.sig_hello;
+  c->off_hello_result = sl.hello_result;
   c->off_gathered = sl.gathered;
   c->pool_last.assign(c->pool, std::make_pair(-1, (uint64_t)0));
   c->sms = sm_count();
@@ -1305,6 +1310,9 @@ zero_status zero_peer_export(zero_ctx* c, void* blob, size_t* blob_bytes) {
   if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
   auto range = get_range_fn();
   if (!range) return c->fail(ZERO_ECUDA, "cuMemGetAddressRange unavailable");
+  // the arenas' zeroing (zero_bind_buffers) must be complete before any peer can
+  // write a signal into them: every rank exports before any rank opens
+  CK(cudaStreamSynchronize(c->stream));
   IpcBlob b{};
   b.magic = kIpcMagic;
   b.rank = (uint32_t)c->rank;
@@ -1364,6 +1372,25 @@ zero_status zero_peer_open(zero_ctx* c, const void* const* blobs, size_t blob_by
     c->peer_grad[r] = reinterpret_cast<uint16_t*>(mapped[0]);
     c->peer_p16[r] = reinterpret_cast<uint16_t*>(mapped[1]);
     c->peer_scratch[r] = reinterpret_cast<char*>(mapped[2]);
+  }
+  // handshake over the new mappings (system-scope release/acquire through every
+  // peer's scratch), bounded so that an unreachable peer is an error, not a hang
+  {
+    uint64_t timeout_ms = 60000;
+    if (const char* ev = getenv("ZERO_PEER_TIMEOUT_MS")) timeout_ms = strtoull(ev, nullptr, 10);
+    SigArgs sa{};
+    for (int j = 0; j < c->n_d; ++j) sa.dst[j] = c->sig(j, c->off_sig_hello, c->rank);
+    sa.n = c->n_d;
+    sa.epoch = 1;
+    uint32_t* dres = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(c->bufs.scratch) + c->off_hello_result);
+    uint32_t hres = 1;
+    CK(launch_handshake(sa, c->sig(c->rank, c->off_sig_hello, 0), timeout_ms * 1000000ull, dres, c->stream));
+    CK(cudaMemcpyAsync(&hres, dres, sizeof(hres), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->launches++;
+    if (hres != 0)
+      return c->fail(ZERO_ECUDA, "peer handshake timed out after %llu ms (a peer did not open its mappings)",
+                     (unsigned long long)timeout_ms);
   }
   c->ipc = true;
   // cross-process: the pull reduce-scatter (NVLink-bound) runs on its own stream so it

@@ -1610,6 +1610,27 @@ __global__ void k_signal(const __grid_constant__ SigArgs a) {
 __global__ void k_wait(const __grid_constant__ WaitArgs a) {
   if (threadIdx.x == 0) wait_all(a.flags, a.n, a.epoch);
 }
+// zero_peer_open's handshake: tell every peer "rank me is linked", then wait (bounded,
+// without trapping) until every peer has said the same; *result = 0 ok, 1 timed out.
+__global__ void k_handshake(const __grid_constant__ SigArgs a, const uint64_t* my_flags, uint64_t timeout_ns,
+                            uint32_t* result) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  for (int j = 0; j < a.n; ++j) st_release_sys(a.dst[j], a.epoch);
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t r = 0;
+  for (int j = 0; j < a.n && !r; ++j)
+    while (ld_acquire_sys(my_flags + j) < a.epoch) {
+      __nanosleep(1000);
+      if (globaltimer_ns() - t0 > timeout_ns) { r = 1; break; }
+    }
+  *result = r;
+}
+cudaError_t launch_handshake(const SigArgs& a, const uint64_t* my_flags, uint64_t timeout_ns, uint32_t* result,
+                             cudaStream_t s) {
+  k_handshake<<<1, 32, 0, s>>>(a, my_flags, timeout_ns, result);
+  return cudaGetLastError();
+}
 __global__ void k_push_partial(const __grid_constant__ PushArgs a) {
   const int j = threadIdx.x;
   if (j < a.n) {

@@ -179,6 +179,8 @@ struct PushArgs {               // copy my partial into every peer's gathered[me
 };
 cudaError_t launch_signal(const SigArgs& a, cudaStream_t s);
 cudaError_t launch_wait(const WaitArgs& a, cudaStream_t s);
+cudaError_t launch_handshake(const SigArgs& a, const uint64_t* my_flags, uint64_t timeout_ns, uint32_t* result,
+                             cudaStream_t s);
 cudaError_t launch_push_partial(const PushArgs& a, cudaStream_t s);
 cudaError_t launch_decide_global(const PartialPtrs& partials, DevState* st, DecideParams p, cudaStream_t s);
 cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int variant);

@@ -203,3 +203,60 @@ def test_torch_training_across_processes(stage):
         msgs.append(q.get())
     assert not hung, f"workers hung: {msgs}"
     assert all(p.exitcode == 0 for p in procs) and msgs == ["ok", "ok"], msgs
+
+
+def _handshake_worker(rank, world, port, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "tests")]
+    try:
+        import time
+        import torch.distributed as dist
+        import synth
+        from paper_1910_02054_b200 import ZeroConfig, ZeroEngine, ZeroError
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), ZERO_PEER_TIMEOUT_MS="2000")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        ts = synth.mlp_layout((64, 32))
+        e = ZeroEngine([t.numel for t in ts], [t.layer for t in ts], world, rank, 1, ZeroConfig.defaults("bf16"),
+                       "peer", align=64, bucket_cap=1 << 12)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, e.peer_export())
+        if rank == 0:
+            t0 = time.time()
+            try:
+                e.peer_open(blobs)
+                q.put("opened without its peer")
+            except ZeroError as exc:
+                dt = time.time() - t0
+                q.put("ok" if ("handshake" in str(exc) and dt < 30) else f"wrong error after {dt:.1f}s: {exc}")
+        dist.barrier()          # rank 1 never opened its mappings
+        if rank == 1:
+            q.put("ok")
+        e.destroy()
+        dist.destroy_process_group()
+    except Exception as exc:  # noqa: BLE001
+        import traceback
+        q.put(f"rank {rank}: {exc!r}\n{traceback.format_exc()}")
+
+
+def test_open_without_peer_times_out():
+    """zero_peer_open's handshake is bounded: a peer that never links is reported as an
+    error within ZERO_PEER_TIMEOUT_MS (bench.py then falls back to NCCL), not a hang."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _port()
+    procs = [ctx.Process(target=_handshake_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+    hung = [p for p in procs if p.is_alive()]
+    for p in hung:
+        p.kill()
+        p.join(10)
+    msgs = []
+    while not q.empty():
+        msgs.append(q.get())
+    assert not hung, f"workers hung: {msgs}"
+    assert sorted(msgs) == ["ok", "ok"], msgs
