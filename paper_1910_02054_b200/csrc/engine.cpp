@@ -187,6 +187,10 @@ struct zero_ctx {
   uint16_t* gather = nullptr;
   DevState* st = nullptr;
   Slot* slots = nullptr;
+  double* cta_sum = nullptr;                       // LOCAL: per-CTA flatten partials per slot
+  uint32_t* cta_flag = nullptr;
+  uint32_t* cta_grid = nullptr;
+  bool flat_pdl = false;                           // ZERO_FLAT_PDL: one flatten stream, PDL-chained launches
   GridPartials* part_compute = nullptr;
   GridPartials* part_flat[4] = {};                 // grid partials per flatten stream
   // LOCAL / NCCL: flattens of consecutive buckets alternate between two library streams
@@ -340,11 +344,12 @@ int grid_for(uint64_t work_items, int per_sm, int sms) {
 // bytes of the scratch arena and the offsets inside it
 struct ScratchLayout {
   size_t st, slots, part_compute, part_flat2, part_flat3, part_flat4, part_comm, my_partial, gathered, segs, sig_flat, sig_rs, sig_part, sig_adam,
-      sig_hello, hello_result, total;
+      sig_hello, hello_result, cta_sum, cta_flag, cta_grid, total;
 };
 // sig_flat[k][r] / sig_rs[k][r]: epoch at which rank r flattened / finished reducing bucket k
 // sig_part[r] / sig_adam[r]: epoch at which rank r published its partial / finished Adam
-ScratchLayout scratch_layout(int n_slots, size_t n_segs, size_t n_buckets) {
+// local: N_d == 1 -- per-CTA flatten epilogue partials for every slot (k_decide_local)
+ScratchLayout scratch_layout(int n_slots, size_t n_segs, size_t n_buckets, bool local) {
   ScratchLayout s{};
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
@@ -364,6 +369,10 @@ ScratchLayout scratch_layout(int n_slots, size_t n_segs, size_t n_buckets) {
   s.sig_adam = take(sizeof(uint64_t) * ZERO_MAX_RANKS);
   s.sig_hello = take(sizeof(uint64_t) * ZERO_MAX_RANKS);   // zero_peer_open's handshake
   s.hello_result = take(sizeof(uint32_t));
+  const size_t ns = local ? (size_t)std::max(n_slots, 1) : 0;
+  s.cta_sum = take(sizeof(double) * kMaxGrid * ns);
+  s.cta_flag = take(sizeof(uint32_t) * kMaxGrid * ns);
+  s.cta_grid = take(sizeof(uint32_t) * ns);
   s.total = o;
   return s;
 }
@@ -557,7 +566,8 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
   if (stage >= 2) z.gred_bytes = (r32 ? 4ull : 2ull) * S;
   else z.gred_bytes = r32 ? 4ull * S : 0;
   z.gather_bytes = (stage == 3 && coll) ? 2ull * (c->cfg.prefetch_depth + 1) * c->max_layer : 0;
-  z.scratch_bytes = scratch_layout(c->n_slots, c->segs_host.size(), c->buckets.size()).total;
+  z.scratch_bytes =
+      scratch_layout(c->n_slots, c->segs_host.size(), c->buckets.size(), c->transport == ZERO_TRANSPORT_LOCAL).total;
 
   c->reduced.assign(c->info.n_buckets, 0);
   c->pool_pending.assign(c->pool, -1);
@@ -596,10 +606,16 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   c->grad = reinterpret_cast<uint16_t*>(b->grad);
   c->gred = b->gred;
   c->gather = reinterpret_cast<uint16_t*>(b->gather);
-  const ScratchLayout sl = scratch_layout(c->n_slots, c->segs_host.size(), c->buckets.size());
+  const ScratchLayout sl =
+      scratch_layout(c->n_slots, c->segs_host.size(), c->buckets.size(), c->transport == ZERO_TRANSPORT_LOCAL);
   char* s = reinterpret_cast<char*>(b->scratch);
   c->st = reinterpret_cast<DevState*>(s + sl.st);
   c->slots = reinterpret_cast<Slot*>(s + sl.slots);
+  if (c->transport == ZERO_TRANSPORT_LOCAL) {
+    c->cta_sum = reinterpret_cast<double*>(s + sl.cta_sum);
+    c->cta_flag = reinterpret_cast<uint32_t*>(s + sl.cta_flag);
+    c->cta_grid = reinterpret_cast<uint32_t*>(s + sl.cta_grid);
+  }
   c->part_compute = reinterpret_cast<GridPartials*>(s + sl.part_compute);
   c->part_flat[0] = c->part_compute;
   c->part_flat[1] = reinterpret_cast<GridPartials*>(s + sl.part_flat2);
@@ -636,6 +652,8 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   } else {
     c->comm_stream = c->stream;
   }
+  if (const char* ev = getenv("ZERO_FLAT_PDL")) c->flat_pdl = atoi(ev) != 0 && c->transport == ZERO_TRANSPORT_LOCAL;
+  if (c->flat_pdl) c->n_flat_streams = 1;
   if (const char* ev = getenv("ZERO_FLAT_STREAMS"))
     c->n_flat_streams = std::max(1, std::min(zero_ctx::kMaxFlatStreams, atoi(ev)));
   c->n_flat_streams_req = c->n_flat_streams;
@@ -862,6 +880,13 @@ zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads, cud
     a.st = c->st;
     a.part = part;
     a.slot = c->slots + slot;
+    if (epi && c->cta_sum) {
+      a.cta_sum = c->cta_sum + (size_t)slot * kMaxGrid;
+      a.cta_flag = c->cta_flag + (size_t)slot * kMaxGrid;
+      a.cta_grid = c->cta_grid + slot;
+    }
+    // chain behind the previous launch of this step's reduce phase on the same stream
+    a.pdl = (c->flat_pdl && (c->n_reduced > 0 || b0 > 0)) ? 1 : 0;
     if (tma_ok) CK(launch_flatten_tma(a, grid, fs, c->flat_tma));
     else CK(launch_flatten(a, grid, fs, c->flat_vecs));
     c->launches++;
@@ -1169,7 +1194,7 @@ zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
   }
   PartialPtrs pp{};
   if (c->transport == ZERO_TRANSPORT_LOCAL) {
-    CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream));
+    CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream, c->cta_sum, c->cta_flag, c->cta_grid));
     c->launches++;
     pp.p[0] = c->my_partial;
   } else if (c->ipc) {  // push my partial into every peer's gathered[rank], then wait for all

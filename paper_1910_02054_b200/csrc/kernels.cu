@@ -247,6 +247,21 @@ __device__ void grid_publish(double s, uint32_t f, GridPartials* part, Slot* slo
   }
 }
 
+// the flatten's N_d = 1 epilogue: per-CTA partials (k_decide_local combines them in a
+// fixed order), or the last-CTA grid combine into the slot
+__device__ __forceinline__ void flat_publish(const FlatArgs& a, double s, uint32_t f) {
+  if (a.cta_sum) {
+    block_reduce(s, f);
+    if (threadIdx.x == 0) {
+      a.cta_sum[blockIdx.x] = s;
+      a.cta_flag[blockIdx.x] = f;
+      if (blockIdx.x == 0) *a.cta_grid = gridDim.x;
+    }
+  } else {
+    grid_publish(s, f, a.part, a.slot);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K2: flatten / cast / prescale one gradient bucket (a1), + epilogue at N_d = 1
 // ---------------------------------------------------------------------------
@@ -298,6 +313,9 @@ template <int SDT, int DDT, bool kCopy, int V>
 __global__ void __launch_bounds__(kThreads, 6) k_flatten(const __grid_constant__ FlatArgs a) {  // <= 40 regs: +1 % (A/B)
   using S = SrcLoad<SDT>;
   using D = H16<DDT>;
+  // PDL: the next bucket's flatten (independent data) may start as soon as every CTA
+  // of this one is resident; a no-op without a programmatic dependent
+  asm volatile("griddepcontrol.launch_dependents;");
   const float sigma = a.sigma;
   const float inv = a.epilogue ? a.st->inv_cur : 0.0f;
   double sumsq = 0.0;
@@ -402,13 +420,32 @@ __global__ void __launch_bounds__(kThreads, 6) k_flatten(const __grid_constant__
     }
     cur = pend;
   }
-  if (a.epilogue) grid_publish(sumsq, flag, a.part, a.slot);
+  if (a.epilogue) flat_publish(a, sumsq, flag);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: complete only after the previous flatten
+}
+
+template <typename Kernel>
+cudaError_t launch_pdl(Kernel kern, int grid, cudaStream_t s, const FlatArgs& a) {
+  if (!a.pdl) {
+    kern<<<grid, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 template <int V>
 cudaError_t launch_flatten_v(const FlatArgs& a, int grid, cudaStream_t s) {
   const bool copy = (a.sigma == 1.0f) && (a.src_dtype == a.dst_dtype);
-#define ZL(SD, DD, CP) k_flatten<SD, DD, CP, V><<<grid, kThreads, 0, s>>>(a)
+#define ZL(SD, DD, CP) launch_pdl(k_flatten<SD, DD, CP, V>, grid, s, a)
   if (a.dst_dtype == DT_F16) {
     if (a.src_dtype == DT_F16) { if (copy) ZL(DT_F16, DT_F16, true); else ZL(DT_F16, DT_F16, false); }
     else if (a.src_dtype == DT_F32) ZL(DT_F32, DT_F16, false);
@@ -559,7 +596,7 @@ __global__ void __launch_bounds__(T / 8 + 32, 1) k_flatten_tma(const __grid_cons
   }
   if (a.epilogue) {
     __syncthreads();
-    grid_publish(sumsq, flag, a.part, a.slot);
+    flat_publish(a, sumsq, flag);
   }
 }
 
@@ -711,7 +748,7 @@ __global__ void __launch_bounds__(T / 8 + 32) k_flatten_tma_st(const __grid_cons
   }
   if (a.epilogue) {
     __syncthreads();
-    grid_publish(sumsq, flag, a.part, a.slot);
+    flat_publish(a, sumsq, flag);
   }
 }
 
@@ -957,7 +994,29 @@ cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s) {
 // slots (ascending bucket, fixed tree) into one RankPartial; decide_global folds
 // the ranks' partials in ascending rank and advances the loss-scale machine.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_decide_local(const Slot* slots, int n, RankPartial* out) {
+__global__ void __launch_bounds__(kThreads) k_decide_local(Slot* slots, int n, RankPartial* out, const double* cta_sum,
+                                                           const uint32_t* cta_flag, const uint32_t* cta_grid) {
+  if (cta_sum) {  // N_d = 1: combine each slot's per-CTA flatten partials (warp per slot, fixed order)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int i = warp; i < n; i += nw) {
+      const uint32_t g = cta_grid[i];
+      const double* cs = cta_sum + (size_t)i * kMaxGrid;
+      const uint32_t* cf = cta_flag + (size_t)i * kMaxGrid;
+      double s = 0.0;
+      uint32_t f = 0;
+      for (uint32_t c = lane; c < g; c += 32) {
+        s += cs[c];
+        f |= cf[c];
+      }
+      s = warp_sum(s);
+      f = __reduce_or_sync(0xffffffffu, f);
+      if (lane == 0) {
+        slots[i].sumsq = s;
+        slots[i].flag = f;
+      }
+    }
+    __syncthreads();
+  }
   double s = 0.0;
   uint32_t f = 0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -971,8 +1030,9 @@ __global__ void __launch_bounds__(kThreads) k_decide_local(const Slot* slots, in
   }
 }
 
-cudaError_t launch_decide_local(const Slot* slots, int n_slots, RankPartial* out, cudaStream_t s) {
-  k_decide_local<<<1, kThreads, 0, s>>>(slots, n_slots, out);
+cudaError_t launch_decide_local(Slot* slots, int n_slots, RankPartial* out, cudaStream_t s, const double* cta_sum,
+                                const uint32_t* cta_flag, const uint32_t* cta_grid) {
+  k_decide_local<<<1, kThreads, 0, s>>>(slots, n_slots, out, cta_sum, cta_flag, cta_grid);
   return cudaGetLastError();
 }
 

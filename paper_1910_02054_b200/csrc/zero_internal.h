@@ -78,6 +78,12 @@ struct FlatArgs {
   const DevState* st;
   GridPartials* part;
   Slot* slot;
+  // N_d == 1: per-CTA epilogue partials of this launch's slot (no last-CTA combine in
+  // the flatten; k_decide_local reduces them in a fixed order); NULL = grid_publish
+  double* cta_sum;
+  uint32_t* cta_flag;
+  uint32_t* cta_grid;
+  int pdl;                  // host: launch as a programmatic dependent of the previous flatten
 };
 
 struct RSArgs {
@@ -153,7 +159,10 @@ cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s, int vecs
 cudaError_t launch_flatten_tma(const FlatArgs& a, int grid, cudaStream_t s, int variant);
 int flatten_tma_ctas_per_sm(int variant);
 cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s);
-cudaError_t launch_decide_local(const Slot* slots, int n_slots, RankPartial* out, cudaStream_t s);
+// cta_*: optional per-CTA flatten partials (N_d == 1), slot i at [i * kMaxGrid, + cta_grid[i])
+cudaError_t launch_decide_local(Slot* slots, int n_slots, RankPartial* out, cudaStream_t s,
+                                const double* cta_sum = nullptr, const uint32_t* cta_flag = nullptr,
+                                const uint32_t* cta_grid = nullptr);
 struct PartialPtrs {
   const RankPartial* p[kMaxRanks];
   const uint64_t* wait_flags;   // cross-process PEER: wait until wait_flags[r] >= epoch

@@ -12,6 +12,7 @@ ap.add_argument("--flat", default="")          # e.g. "4x4,4x8"  (vecs x ctas)
 ap.add_argument("--base", default="")          # fixed env for every run, e.g. "ZERO_ADAM_VARIANT=1"
 ap.add_argument("--flat-tma", default="")      # e.g. "1,2,3,4"
 ap.add_argument("--flat-streams", default="")  # e.g. "1,2,3,4"
+ap.add_argument("--env", default="")           # free-form variants: "A=1,B=2|A=0" (one variant per '|')
 args, extra = ap.parse_known_args()
 base = dict(kv.split("=") for kv in args.base.split(",") if kv)
 variants = []
@@ -24,6 +25,8 @@ for fs in [x for x in args.flat_streams.split(",") if x]:
     variants.append(dict(base, ZERO_FLAT_STREAMS=fs))
 for ft in [x for x in args.flat_tma.split(",") if x]:
     variants.append(dict(base, ZERO_FLAT_TMA=ft))
+for ev in [x for x in args.env.split("|") if x]:
+    variants.append(dict(base, **dict(kv.split("=") for kv in ev.split(",") if kv)))
 for v in variants:
     env = dict(os.environ, **v)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "30", "--no-e2e",
