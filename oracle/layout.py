@@ -17,6 +17,11 @@ The concrete rule is reading c-7:
   whenever the next A-aligned start has no room; a tensor that does not fit is
   split at cap; each bucket is padded to a multiple of Q; rank r owns the r-th
   1/N slice of every bucket.
+  ZeRO x MP (reading R-MP1): an optional per-tensor group (1 = the
+  tensor is replicated across the model-parallel group, 0 = MP-partitioned) also
+  starts a new bucket when it changes, so no bucket mixes the two (a bucket's
+  gradient-norm contribution is then either counted on every MP rank or only on
+  MP rank 0).  With no groups the layout is unchanged.
 
 Pins (tests/test_oracle_layout.py): SPEC make_layout examples (S:347-349:
 (10,4) -> 12 with ranges [0,3),[3,6),[6,9),[9,12); (8,1) -> [0,8); (7,2) -> 8) as
@@ -41,6 +46,7 @@ class Piece:
 @dataclasses.dataclass
 class Bucket:
     layer: int
+    group: int = 0    # R-MP1: 1 = MP-replicated tensors
     base: int = 0     # global flat offset
     size: int = 0     # B_k (padded, multiple of N*A)
     used: int = 0
@@ -80,7 +86,7 @@ def _align_up(x: int, a: int) -> int:
 
 
 def make_layout(numels: Sequence[int], layers: Sequence[int], n_d: int, align: int,
-                bucket_cap: int) -> Layout:
+                bucket_cap: int, groups: Sequence[int] = None) -> Layout:
     if n_d < 1 or align < 1 or (align & (align - 1)) != 0:
         raise ValueError("n_d >= 1 and align a power of two required")
     Q = n_d * align
@@ -103,17 +109,19 @@ def make_layout(numels: Sequence[int], layers: Sequence[int], n_d: int, align: i
     for t, (n, L) in enumerate(zip(numels, layers)):
         if n == 0:
             continue
-        if cur.used > 0 and L != cur.layer:
+        G = groups[t] if groups is not None else 0
+        if cur.used > 0 and (L != cur.layer or G != cur.group):
             close(cur)
-            cur = Bucket(layer=L)
-        cur.layer = L if cur.used == 0 else cur.layer
+            cur = Bucket(layer=L, group=G)
+        if cur.used == 0:
+            cur.layer, cur.group = L, G
         rem, toff = n, 0
         while rem > 0:
             start = _align_up(cur.used, align)
             room = (cap - start) if cap is not None else rem
             if room <= 0:
                 close(cur)
-                cur = Bucket(layer=L)
+                cur = Bucket(layer=L, group=G)
                 continue
             take = min(rem, room)
             cur.pieces.append(Piece(t, toff, start, take))
@@ -122,7 +130,7 @@ def make_layout(numels: Sequence[int], layers: Sequence[int], n_d: int, align: i
             toff += take
             if rem > 0:
                 close(cur)
-                cur = Bucket(layer=L)
+                cur = Bucket(layer=L, group=G)
     close(cur)
 
     base = 0

@@ -35,8 +35,8 @@ def test_config1_table(golden):
     assert got == g["buckets"]
 
 
-def _check_properties(numels, layers, n, a, cb):
-    lay = L.make_layout(numels, layers, n, a, cb)
+def _check_properties(numels, layers, n, a, cb, groups=None):
+    lay = L.make_layout(numels, layers, n, a, cb, groups)
     Q = n * a
     psi = sum(numels)
     cover = np.zeros(lay.psi_padded, np.int32)
@@ -47,6 +47,8 @@ def _check_properties(numels, layers, n, a, cb):
         if cb:
             assert b.size <= cb // Q * Q
         assert all(layers[p.tensor] == b.layer for p in b.pieces)       # never spans layers
+        if groups is not None:                                            # R-MP1: never mixes groups
+            assert all(groups[p.tensor] == b.group for p in b.pieces)
         for p in b.pieces:
             assert p.bucket_off % a == 0                                  # A-aligned starts
             assert p.bucket_off + p.count <= b.size
@@ -114,3 +116,42 @@ def test_paper_layouts_counts():
         ts = synth.CONFIGS[name]()
         lay = L.make_layout([t.numel for t in ts], [t.layer for t in ts], n, 64, 1 << 26)
         assert (len(ts), lay.psi_padded, len(lay.buckets), lay.shard) == (nt, pp, nb, shard)
+
+
+def test_mp_groups_split_like_layers():
+    """Reading R-MP1: a change of MP group (replicated vs partitioned tensor) closes a
+    bucket exactly as a layer change does, so the grouped layout equals the plain
+    layout of the same tensors with every maximal same-(layer, group) run given its
+    own layer id; all-zero groups change nothing."""
+    rnd = random.Random(99)
+    for _ in range(800):
+        nt = rnd.randint(1, 14)
+        numels = [rnd.choice([0, 1, 5, 64, 65, 300]) if rnd.random() < 0.4 else rnd.randint(1, 2000)
+                  for _ in range(nt)]
+        if sum(numels) == 0:
+            numels[0] = 3
+        layers, L_ = [], 0
+        for _t in range(nt):
+            if rnd.random() < 0.25:
+                L_ += 1
+            layers.append(L_)
+        groups = [rnd.randint(0, 1) for _ in range(nt)]
+        n = rnd.choice([1, 2, 4, 8])
+        a = rnd.choice([1, 8, 64])
+        Q = n * a
+        cb = rnd.choice([0, Q, 5 * Q, rnd.randint(Q, 30 * Q)])
+        lay = _check_properties(numels, layers, n, a, cb, groups)
+        # relabel: a new pseudo-layer at every (layer, group) change among non-empty tensors
+        pseudo, cur, key = [], -1, None
+        for t in range(nt):
+            k = (layers[t], groups[t])
+            if numels[t] > 0 and k != key:
+                cur, key = cur + 1, k
+            pseudo.append(max(cur, 0))
+        ref = L.make_layout(numels, pseudo, n, a, cb)
+        assert [(b.base, b.size, [(p.tensor, p.tensor_off, p.bucket_off, p.count) for p in b.pieces])
+                for b in lay.buckets] == [(b.base, b.size, [(p.tensor, p.tensor_off, p.bucket_off, p.count)
+                                                            for p in b.pieces]) for b in ref.buckets]
+        plain = L.make_layout(numels, layers, n, a, cb)
+        zero = L.make_layout(numels, layers, n, a, cb, [0] * nt)
+        assert [(b.base, b.size, b.layer) for b in plain.buckets] == [(b.base, b.size, b.layer) for b in zero.buckets]
