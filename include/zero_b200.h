@@ -73,14 +73,21 @@ typedef enum { ZERO_TRANSPORT_LOCAL = 0, ZERO_TRANSPORT_NCCL = 1, ZERO_TRANSPORT
  * Parameter layout (reading c-7; "N_d equal partitions", P:366 buckets,
  * P:420-422 constant-size buffer C_B).
  * Tensors are listed in forward order with non-decreasing layer ids.  Tensor t
- * is placed in buckets that never span layers; every bucket is padded to a
+ * is placed in buckets that never span layers (nor MP-replicated and partitioned
+ * tensors, see ZERO_TENSOR_MP_REPLICATED); every bucket is padded to a
  * multiple of N_d * align_elems; rank r owns the r-th 1/N_d slice of every
  * bucket, so each rank owns exactly psi_padded / N_d elements.
  * ------------------------------------------------------------------------- */
+/* zero_tensor.flags: the tensor is replicated across a model-parallel group (e.g.
+ * LayerNorm weights and row-parallel biases under Megatron tensor slicing):
+ * its gradient-norm contribution counts only on MP rank 0 (zero_config.mp_rank), and
+ * no bucket mixes replicated and MP-partitioned tensors (reading R-MP1). */
+#define ZERO_TENSOR_MP_REPLICATED 1u
+
 typedef struct {
   uint64_t numel;   /* elements of the tensor (0 allowed: the tensor is skipped) */
   uint32_t layer;   /* layer id, non-decreasing in forward order */
-  uint32_t reserved;
+  uint32_t flags;   /* ZERO_TENSOR_MP_REPLICATED or 0 */
 } zero_tensor;
 
 typedef struct {
@@ -94,7 +101,7 @@ typedef struct {
   uint32_t layer;
   uint32_t n_pieces;
   uint32_t first_piece;        /* index into the piece array */
-  uint32_t reserved;
+  uint32_t flags;              /* ZERO_TENSOR_MP_REPLICATED if its tensors are */
   uint64_t base;               /* global flat offset of the bucket */
   uint64_t size;               /* B_k: padded size, multiple of N_d * A */
   uint64_t shard_off;          /* offset of this bucket's slice in every rank's shard */

@@ -61,33 +61,35 @@ bool plan(const zero_layout_desc* d, int n_d, LayoutResult& out) {
   for (uint32_t t = 1; t < d->n_tensors; ++t)
     if (d->tensors[t].layer < d->tensors[t - 1].layer) { out.error = "layer ids must be non-decreasing"; return false; }
 
-  struct Cur { uint32_t layer; uint64_t used; std::vector<zero_piece> p; } cur{0, 0, {}};
+  // a bucket never spans layers, nor MP-replicated and MP-partitioned tensors (R-MP1)
+  struct Cur { uint32_t layer, flags; uint64_t used; std::vector<zero_piece> p; } cur{0, 0, 0, {}};
   bool have_layer = false;
   std::vector<Cur> closed;
   auto close = [&](uint32_t next_layer) {
     if (cur.used > 0) closed.push_back(cur);
-    cur = Cur{next_layer, 0, {}};
+    cur = Cur{next_layer, 0, 0, {}};
   };
   uint64_t psi = 0;
   for (uint32_t t = 0; t < d->n_tensors; ++t) {
     const uint64_t n = d->tensors[t].numel;
     const uint32_t L = d->tensors[t].layer;
+    const uint32_t F = d->tensors[t].flags & ZERO_TENSOR_MP_REPLICATED;
     if (n == 0) continue;
     psi += n;
     if (!have_layer) { cur.layer = L; have_layer = true; }
-    if (cur.used > 0 && L != cur.layer) close(L);
-    if (cur.used == 0) cur.layer = L;
+    if (cur.used > 0 && (L != cur.layer || F != cur.flags)) close(L);
+    if (cur.used == 0) { cur.layer = L; cur.flags = F; }
     uint64_t rem = n, toff = 0;
     while (rem > 0) {
       const uint64_t start = align_up(cur.used, A);
-      if (cap && start >= cap) { close(L); continue; }
+      if (cap && start >= cap) { close(L); cur.flags = F; continue; }
       const uint64_t room = cap ? cap - start : rem;
       const uint64_t take = std::min(rem, room);
       cur.p.push_back(zero_piece{t, 0, toff, start, take});
       cur.used = start + take;
       rem -= take;
       toff += take;
-      if (rem > 0) close(L);
+      if (rem > 0) { close(L); cur.flags = F; }
     }
   }
   close(0);
@@ -98,6 +100,7 @@ bool plan(const zero_layout_desc* d, int n_d, LayoutResult& out) {
   for (size_t k = 0; k < closed.size(); ++k) {
     zero_bucket b{};
     b.layer = closed[k].layer;
+    b.flags = closed[k].flags;
     b.size = align_up(closed[k].used, Q);
     b.base = base;
     b.shard_off = shard_off;

@@ -23,6 +23,7 @@ _LIB_PATH = os.environ.get("ZERO_LIB_PATH") or os.path.join(_PKG, "libzero_b200.
 # ABI structs (mirror include/zero_b200.h field by field)
 # ---------------------------------------------------------------------------
 FP16, BF16, FP32 = 0, 1, 2
+MP_REPLICATED = 1          # zero_tensor.flags: replicated across the MP group (reading R-MP1)
 R16, R32 = 0, 1
 TRANSPORT = {"local": 0, "nccl": 1, "peer": 2}
 STATUS = {0: "ZERO_OK", 1: "ZERO_EINVAL", 2: "ZERO_ENOMEM", 3: "ZERO_ECUDA", 4: "ZERO_ENCCL",
@@ -31,7 +32,7 @@ Q_LAYOUT, Q_MEMORY, Q_COMM, Q_STEP, Q_BUCKETS, Q_PIECES, Q_STATE, Q_TIMING = ran
 
 
 class CTensor(C.Structure):
-    _fields_ = [("numel", C.c_uint64), ("layer", C.c_uint32), ("reserved", C.c_uint32)]
+    _fields_ = [("numel", C.c_uint64), ("layer", C.c_uint32), ("flags", C.c_uint32)]
 
 
 class CLayoutDesc(C.Structure):
@@ -41,7 +42,7 @@ class CLayoutDesc(C.Structure):
 
 class CBucket(C.Structure):
     _fields_ = [("layer", C.c_uint32), ("n_pieces", C.c_uint32), ("first_piece", C.c_uint32),
-                ("reserved", C.c_uint32), ("base", C.c_uint64), ("size", C.c_uint64), ("shard_off", C.c_uint64)]
+                ("flags", C.c_uint32), ("base", C.c_uint64), ("size", C.c_uint64), ("shard_off", C.c_uint64)]
 
 
 class CPiece(C.Structure):
@@ -219,15 +220,17 @@ class ZeroConfig:
                        1 if self.timing else 0)
 
 
-def _desc(numels: Sequence[int], layers: Sequence[int], align: int, bucket_cap: int):
-    arr = (CTensor * len(numels))(*[CTensor(int(n), int(L), 0) for n, L in zip(numels, layers)])
+def _desc(numels: Sequence[int], layers: Sequence[int], align: int, bucket_cap: int, flags=None):
+    fl = flags if flags is not None else [0] * len(numels)
+    arr = (CTensor * len(numels))(*[CTensor(int(n), int(L), int(f)) for n, L, f in zip(numels, layers, fl)])
     d = CLayoutDesc(len(numels), align, arr, bucket_cap)
     return d, arr
 
 
-def plan_layout(numels, layers, n_d: int, align: int = 64, bucket_cap: int = 1 << 26):
-    """zero_plan_layout: (info, buckets, pieces) as Python objects. Pure host call."""
-    d, keep = _desc(numels, layers, align, bucket_cap)
+def plan_layout(numels, layers, n_d: int, align: int = 64, bucket_cap: int = 1 << 26, flags=None):
+    """zero_plan_layout: (info, buckets, pieces) as Python objects. Pure host call.
+    flags: per tensor, MP_REPLICATED (1) or 0."""
+    d, keep = _desc(numels, layers, align, bucket_cap, flags)
     info = CLayoutInfo()
     _check(lib.zero_plan_layout(C.byref(d), n_d, C.byref(info), None, 0, None, 0))
     bk = (CBucket * info.n_buckets)()
@@ -260,15 +263,16 @@ class ZeroEngine:
     def __init__(self, numels: Sequence[int], layers: Sequence[int], n_d: int = 1, rank: int = 0,
                  stage: int = 1, config: Optional[ZeroConfig] = None, transport: str = "local",
                  nccl_comm: int = 0, stream: Optional[torch.cuda.Stream] = None, align: int = 64,
-                 bucket_cap: int = 1 << 26, device=None, bind: bool = True):
+                 bucket_cap: int = 1 << 26, device=None, bind: bool = True, flags=None):
         self.config = config or ZeroConfig()
         self.numels = [int(n) for n in numels]
         self.layers = [int(L) for L in layers]
+        self.flags = [int(f) for f in flags] if flags is not None else None
         self.n_d, self.rank, self.stage = n_d, rank, stage
         self.device = torch.device(device) if device is not None else (
             torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None)
         self.stream = stream
-        d, keep = _desc(self.numels, self.layers, align, bucket_cap)
+        d, keep = _desc(self.numels, self.layers, align, bucket_cap, self.flags)
         ctx = C.c_void_p()
         cs = stream.cuda_stream if stream is not None else (
             torch.cuda.current_stream(self.device).cuda_stream if bind else 0)
@@ -473,10 +477,10 @@ class ZeroSimGroup:
     the production kernels run over a same-device peer-pointer table."""
 
     def __init__(self, numels, layers, n_d: int, stage: int, config: Optional[ZeroConfig] = None,
-                 align: int = 64, bucket_cap: int = 1 << 26, stream=None, device=None):
+                 align: int = 64, bucket_cap: int = 1 << 26, stream=None, device=None, flags=None):
         stream = stream or torch.cuda.current_stream(device)
-        self.ranks = [ZeroEngine(numels, layers, n_d, r, stage, config, "peer", 0, stream, align, bucket_cap, device)
-                      for r in range(n_d)]
+        self.ranks = [ZeroEngine(numels, layers, n_d, r, stage, config, "peer", 0, stream, align, bucket_cap, device,
+                                 flags=flags) for r in range(n_d)]
         arr = (C.c_void_p * n_d)(*[e._ctx.value for e in self.ranks])
         _check(lib.zero_sim_group(arr, n_d), self.ranks[0]._ctx)
 

@@ -46,9 +46,9 @@ def test_library_built_for_sm100a():
     assert "sm_100a" in out
 
 
-def _cmp_layout(z, numels, layers, n, a, cb):
-    ol = OL.make_layout(numels, layers, n, a, cb)
-    info, bk, pc = z.plan_layout(numels, layers, n, a, cb)
+def _cmp_layout(z, numels, layers, n, a, cb, groups=None):
+    ol = OL.make_layout(numels, layers, n, a, cb, groups)
+    info, bk, pc = z.plan_layout(numels, layers, n, a, cb, flags=groups)
     assert info.psi == ol.psi and info.psi_padded == ol.psi_padded and info.shard == ol.shard
     assert info.n_buckets == len(ol.buckets)
     got = []
@@ -58,6 +58,7 @@ def _cmp_layout(z, numels, layers, n, a, cb):
     want = [(b.layer, b.base, b.size, b.shard_off, [(p.tensor, p.tensor_off, p.bucket_off, p.count) for p in b.pieces])
             for b in ol.buckets]
     assert got == want
+    assert [b.flags for b in bk] == [b.group for b in ol.buckets]
 
 
 def test_layout_matches_oracle_random(z):
@@ -153,3 +154,22 @@ def test_comm_volume_closed_forms(z, n, stage):
     info, _, _ = z.plan_layout([t.numel for t in ts], [t.layer for t in ts], n, 64, 1 << 26)
     got = z.comm_elems_per_rank(info.psi_padded, n, stage)
     assert got == P.step_elems_per_rank(info.psi_padded, n, stage)
+
+
+def test_layout_mp_groups_match_oracle(z):
+    """ZERO_TENSOR_MP_REPLICATED splits buckets exactly as the oracle's groups (R-MP1)."""
+    rnd = random.Random(7)
+    for _ in range(400):
+        nt = rnd.randint(1, 12)
+        numels = [rnd.choice([0, 1, 64, 65, 1000]) if rnd.random() < 0.4 else rnd.randint(1, 4000) for _ in range(nt)]
+        if sum(numels) == 0:
+            numels[-1] = 3
+        layers, L = [], 0
+        for _t in range(nt):
+            L += rnd.random() < 0.3
+            layers.append(L)
+        groups = [rnd.randint(0, 1) for _ in range(nt)]
+        n = rnd.choice([1, 2, 4, 8])
+        a = rnd.choice([1, 8, 64])
+        cb = rnd.choice([0, n * a, rnd.randint(n * a, 20 * n * a)])
+        _cmp_layout(z, numels, layers, n, a, cb, groups)
