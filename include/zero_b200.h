@@ -157,6 +157,9 @@ typedef struct {
   uint32_t prefetch_depth;     /* stage 3: layers gathered ahead of use (default 1) */
   uint32_t pool_buckets;       /* stages 2/3, N_d > 1: C_B staging slots (default 2) */
   uint32_t timing;             /* 1: record CUDA events around each phase (ZERO_Q_TIMING) */
+  uint32_t mp_rank;            /* ZeRO x MP: this rank's index in its model-parallel group
+                                  (0 without MP); MP-replicated tensors add to the
+                                  gradient norm only on MP rank 0 (R-MP1) */
 } zero_config;
 
 /* Step record (32 bytes), written asynchronously by zero_step. */
@@ -306,6 +309,23 @@ zero_status zero_reduce_grads(struct zero_ctx* ctx, uint32_t bucket, const void*
  * simulated group, not reduced by every rank; or the rank already stepped). */
 zero_status zero_step(struct zero_ctx* ctx, zero_step_info* host_out);
 
+/* ZeRO x MP (reading R-MP1): zero_step in two halves, so that the step
+ * decision can span the model-parallel group as well as this data-parallel one.
+ * zero_step_begin does everything zero_step does up to the decision: it joins the
+ * reduce phase and writes this DP group's combined partial {sum of (G*inv)^2 over
+ * the counted buckets, number of ranks with a non-finite gradient} (two doubles) to
+ * the device address zero_query(ZERO_Q_DECISION) returns; the caller's compute
+ * stream is ordered after the write.  The caller then SUM-all-reduces those 16 bytes
+ * over its MP group on the compute stream (e.g. torch.distributed.all_reduce of a
+ * float64 view), so every MP rank sees the global norm and the global overflow, and
+ * calls zero_step_end, which makes the decision from the (all-reduced) partial and
+ * finishes the step exactly as zero_step.  Without MP, zero_step_begin followed by
+ * zero_step_end is zero_step.  Buckets of MP-replicated tensors
+ * (ZERO_TENSOR_MP_REPLICATED) add to the norm only on MP rank 0 (zero_config.mp_rank).
+ * Errors: as zero_step; ZERO_ESTATE for a begin without end or the reverse. */
+zero_status zero_step_begin(struct zero_ctx* ctx);
+zero_status zero_step_end(struct zero_ctx* ctx, zero_step_info* host_out);
+
 /* Stage 3: make layer `layer`'s 16-bit parameters available (all-gather of its
  * buckets into a pool slot, "spread ... across the entire forward
  * propagation ... once again for the backward propagation in the reverse order")
@@ -333,8 +353,11 @@ enum {
   ZERO_Q_BUCKETS = 4,     /* out: zero_bucket[n_buckets] */
   ZERO_Q_PIECES = 5,      /* out: zero_piece[n_pieces] */
   ZERO_Q_STATE = 6,       /* out: zero_device_state (synchronizes) */
-  ZERO_Q_TIMING = 7       /* out: zero_timing, accumulated since the last TIMING query
+  ZERO_Q_TIMING = 7,      /* out: zero_timing, accumulated since the last TIMING query
                              (synchronizes; needs cfg.timing = 1), then reset */
+  ZERO_Q_DECISION = 8     /* out: void*, the device address of the 16-byte decision
+                             partial {double sum_sq, double overflow} that
+                             zero_step_begin writes (see zero_step_begin) */
 };
 typedef struct {          /* persistent model-state bytes on this rank (Fig. 1 categories) */
   uint64_t params16, grads16, optimizer, reduced_grad_extra, staging, gather_pool, scratch;

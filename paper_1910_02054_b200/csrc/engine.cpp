@@ -194,6 +194,13 @@ struct zero_ctx {
   uint32_t* cta_flag = nullptr;
   uint32_t* cta_grid = nullptr;
   bool flat_pdl = false;                           // ZERO_FLAT_PDL: one flatten stream, PDL-chained launches
+  // ZeRO x MP (R-MP1): per-slot norm weights (0 for MP-replicated buckets on MP rank > 0)
+  double* slot_w = nullptr;
+  std::vector<double> slot_w_host;
+  bool use_slot_w = false;
+  RankPartial* dp_partial = nullptr;               // zero_step_begin's data-parallel sum
+  bool step_begun = false;
+  int pend_ev = -1;
   GridPartials* part_compute = nullptr;
   GridPartials* part_flat[4] = {};                 // grid partials per flatten stream
   // LOCAL / NCCL: flattens of consecutive buckets alternate between two library streams
@@ -347,7 +354,7 @@ int grid_for(uint64_t work_items, int per_sm, int sms) {
 // bytes of the scratch arena and the offsets inside it
 struct ScratchLayout {
   size_t st, slots, part_compute, part_flat2, part_flat3, part_flat4, part_comm, my_partial, gathered, segs, sig_flat, sig_rs, sig_part, sig_adam,
-      sig_hello, hello_result, cta_sum, cta_flag, cta_grid, total;
+      sig_hello, hello_result, cta_sum, cta_flag, cta_grid, slot_w, dp_partial, total;
 };
 // sig_flat[k][r] / sig_rs[k][r]: epoch at which rank r flattened / finished reducing bucket k
 // sig_part[r] / sig_adam[r]: epoch at which rank r published its partial / finished Adam
@@ -376,6 +383,8 @@ ScratchLayout scratch_layout(int n_slots, size_t n_segs, size_t n_buckets, bool 
   s.cta_sum = take(sizeof(double) * kMaxGrid * ns);
   s.cta_flag = take(sizeof(uint32_t) * kMaxGrid * ns);
   s.cta_grid = take(sizeof(uint32_t) * ns);
+  s.slot_w = take(sizeof(double) * (size_t)std::max(n_slots, 1));
+  s.dp_partial = take(sizeof(RankPartial));
   s.total = o;
   return s;
 }
@@ -534,6 +543,12 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
     slots += (int)((c->flat_tmpl[k].size() + kMaxFlatPieces - 1) / kMaxFlatPieces);
   }
   c->n_slots = slots;
+  c->slot_w_host.assign((size_t)std::max(slots, 1), 1.0);
+  for (uint32_t k = 0; k < c->info.n_buckets; ++k) {
+    const int s1 = k + 1 < c->info.n_buckets ? c->slot_base[k + 1] : slots;
+    if ((c->buckets[k].flags & ZERO_TENSOR_MP_REPLICATED) && c->cfg.mp_rank != 0)
+      for (int s = c->slot_base[k]; s < s1; ++s) { c->slot_w_host[s] = 0.0; c->use_slot_w = true; }
+  }
 
   // Adam segments over this rank's local index space
   c->S_e = stage == 0 ? c->info.psi_padded : c->info.shard;
@@ -614,6 +629,8 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   char* s = reinterpret_cast<char*>(b->scratch);
   c->st = reinterpret_cast<DevState*>(s + sl.st);
   c->slots = reinterpret_cast<Slot*>(s + sl.slots);
+  c->slot_w = reinterpret_cast<double*>(s + sl.slot_w);
+  c->dp_partial = reinterpret_cast<RankPartial*>(s + sl.dp_partial);
   if (c->transport == ZERO_TRANSPORT_LOCAL) {
     c->cta_sum = reinterpret_cast<double*>(s + sl.cta_sum);
     c->cta_flag = reinterpret_cast<uint32_t*>(s + sl.cta_flag);
@@ -680,6 +697,8 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   const uint64_t sz[6] = {z.opt_bytes, z.p16_bytes, z.grad_bytes, z.gred_bytes, z.gather_bytes, z.scratch_bytes};
   for (int i = 0; i < 6; ++i)
     if (sz[i]) CK(cudaMemsetAsync(const_cast<void*>(ptrs[i]), 0, sz[i], c->stream));
+  CK(cudaMemcpyAsync(c->slot_w, c->slot_w_host.data(), sizeof(double) * c->slot_w_host.size(), cudaMemcpyHostToDevice,
+                     c->stream));
   CK(cudaMemcpyAsync(c->segs, c->segs_host.data(), sizeof(AdamSeg) * c->segs_host.size(), cudaMemcpyHostToDevice,
                      c->stream));
   const float inv = (float)(1.0 / ((double)c->n_d * (double)c->cfg.loss_scale * (double)c->cfg.grad_prescale));
@@ -1062,7 +1081,8 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
       if (++g->reduced_buckets == c->info.n_buckets) {
         for (int j = 0; j < g->n; ++j) {
           zero_ctx* cj = g->ranks[j];
-          if (launch_decide_local(cj->slots, cj->n_slots, cj->my_partial, cj->comm_stream) != cudaSuccess)
+          if (launch_decide_local(cj->slots, cj->n_slots, cj->my_partial, cj->comm_stream,
+                                  cj->use_slot_w ? cj->slot_w : nullptr) != cudaSuccess)
             return cj->fail(ZERO_ECUDA, "decide_local launch failed");
           cj->launches++;
         }
@@ -1168,10 +1188,15 @@ void reset_step(zero_ctx* c) {
 
 extern "C" {
 
-zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
-  STICKY(c);
-  NvtxRange nvtx("zero_step");
+}  // extern "C"
+
+namespace {
+
+// zero_step, first half: join the reduce phase and form the decision inputs (the
+// per-rank {sum of squares, overflow} partials, exchanged across the data-parallel group)
+zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev) {
   if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
+  if (c->step_begun) return c->fail(ZERO_ESTATE, "zero_step_begin already issued: finish with zero_step_end");
   ZeroGroup* g = c->group;
   if (g) {
     if (g->reduced_buckets != c->info.n_buckets)
@@ -1190,18 +1215,20 @@ zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
     if (c->comm_stream != c->stream) CK(cudaStreamWaitEvent(c->stream, c->ev_join[i], 0));
     c->flat_used[i] = false;
   }
-  zero_ctx::StepEvents* ev = nullptr;
+  ev = nullptr;
   if (c->cfg.timing && c->step_open) {
     ev = &c->ev_pool[c->ev_used];
     CK(cudaEventRecord(ev->r1, c->comm_stream));
   }
-  PartialPtrs pp{};
+  pp = PartialPtrs{};
   if (c->transport == ZERO_TRANSPORT_LOCAL) {
-    CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream, c->cta_sum, c->cta_flag, c->cta_grid));
+    CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream, c->use_slot_w ? c->slot_w : nullptr,
+                           c->cta_sum, c->cta_flag, c->cta_grid));
     c->launches++;
     pp.p[0] = c->my_partial;
+    pp.n = 1;
   } else if (c->ipc) {  // push my partial into every peer's gathered[rank], then wait for all
-    CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream));
+    CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream, c->use_slot_w ? c->slot_w : nullptr));
     c->launches++;
     PushArgs pa{};
     pa.mine = c->my_partial;
@@ -1214,16 +1241,25 @@ zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
     CK(launch_push_partial(pa, c->comm_stream));
     c->launches++;
     for (int j = 0; j < c->n_d; ++j) pp.p[j] = c->gathered + j;
+    pp.n = c->n_d;
     pp.wait_flags = c->sig(c->rank, c->off_sig_part, 0);
     pp.epoch = c->epoch();
   } else if (c->transport == ZERO_TRANSPORT_PEER) {
     for (int j = 0; j < g->n; ++j) pp.p[j] = g->ranks[j]->my_partial;
+    pp.n = g->n;
   } else {
-    CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream));
+    CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream, c->use_slot_w ? c->slot_w : nullptr));
     c->launches++;
     NK(ncclAllGather(c->my_partial, c->gathered, 2, ncclFloat64, c->comm, c->comm_stream));
     for (int j = 0; j < c->n_d; ++j) pp.p[j] = c->gathered + j;
+    pp.n = c->n_d;
   }
+  return ZERO_OK;
+}
+
+// zero_step, second half: decision, fused Adam + recast, all-gather, bookkeeping
+zero_status step_finish(zero_ctx* c, const PartialPtrs& pp, zero_ctx::StepEvents* ev, zero_step_info* host_out) {
+  ZeroGroup* g = c->group;
   CK(launch_decide_global(pp, c->st, decide_params(c), c->comm_stream));
   c->launches++;
   if (ev) CK(cudaEventRecord(ev->a0, c->comm_stream));
@@ -1291,6 +1327,55 @@ zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
     reset_step(c);
   }
   return ZERO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
+  STICKY(c);
+  NvtxRange nvtx("zero_step");
+  PartialPtrs pp{};
+  zero_ctx::StepEvents* ev = nullptr;
+  zero_status s = step_inputs(c, pp, ev);
+  if (s != ZERO_OK) return s;
+  return step_finish(c, pp, ev, host_out);
+}
+
+zero_status zero_step_begin(zero_ctx* c) {
+  STICKY(c);
+  NvtxRange nvtx("zero_step_begin");
+  PartialPtrs pp{};
+  zero_ctx::StepEvents* ev = nullptr;
+  zero_status s = step_inputs(c, pp, ev);
+  if (s != ZERO_OK) return s;
+  CK(launch_combine_partials(pp, c->dp_partial, c->comm_stream));
+  c->launches++;
+  if (c->comm_stream != c->stream) {  // the caller's exchange runs on its stream
+    CK(cudaEventRecord(c->ev_step, c->comm_stream));
+    CK(cudaStreamWaitEvent(c->stream, c->ev_step, 0));
+  }
+  c->pend_ev = ev ? (int)(ev - c->ev_pool.data()) : -1;
+  c->step_begun = true;
+  return ZERO_OK;
+}
+
+zero_status zero_step_end(zero_ctx* c, zero_step_info* host_out) {
+  STICKY(c);
+  NvtxRange nvtx("zero_step_end");
+  if (!c->step_begun) return c->fail(ZERO_ESTATE, "zero_step_end without zero_step_begin");
+  if (c->comm_stream != c->stream) {  // after the caller's exchange of the partial
+    CK(cudaEventRecord(c->ev_step, c->stream));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_step, 0));
+  }
+  PartialPtrs pp{};
+  pp.p[0] = c->dp_partial;
+  pp.n = 1;
+  zero_ctx::StepEvents* ev = c->pend_ev >= 0 ? &c->ev_pool[c->pend_ev] : nullptr;
+  c->step_begun = false;
+  c->pend_ev = -1;
+  return step_finish(c, pp, ev, host_out);
 }
 
 // ---------------------------------------------------------------------------
@@ -1674,6 +1759,12 @@ zero_status zero_query(const zero_ctx* cc, int what, void* out, size_t n) {
       tm.kernel_launches = c->launches;
       tm.adam_launches = c->adam_launches;
       *reinterpret_cast<zero_timing*>(out) = tm;
+      return ZERO_OK;
+    }
+    case ZERO_Q_DECISION: {
+      if (n < sizeof(void*)) return ZERO_EINVAL;
+      if (!c->bound) return ZERO_ESTATE;
+      *reinterpret_cast<void**>(out) = c->dp_partial;
       return ZERO_OK;
     }
     default:

@@ -994,8 +994,9 @@ cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s) {
 // slots (ascending bucket, fixed tree) into one RankPartial; decide_global folds
 // the ranks' partials in ascending rank and advances the loss-scale machine.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_decide_local(Slot* slots, int n, RankPartial* out, const double* cta_sum,
-                                                           const uint32_t* cta_flag, const uint32_t* cta_grid) {
+__global__ void __launch_bounds__(kThreads) k_decide_local(Slot* slots, int n, RankPartial* out, const double* slot_w,
+                                                           const double* cta_sum, const uint32_t* cta_flag,
+                                                           const uint32_t* cta_grid) {
   if (cta_sum) {  // N_d = 1: combine each slot's per-CTA flatten partials (warp per slot, fixed order)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int i = warp; i < n; i += nw) {
@@ -1020,7 +1021,7 @@ __global__ void __launch_bounds__(kThreads) k_decide_local(Slot* slots, int n, R
   double s = 0.0;
   uint32_t f = 0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    s += slots[i].sumsq;
+    s += slot_w ? slot_w[i] * slots[i].sumsq : slots[i].sumsq;  // weights 0/1: exact
     f |= slots[i].flag;
   }
   block_reduce(s, f);
@@ -1030,17 +1031,34 @@ __global__ void __launch_bounds__(kThreads) k_decide_local(Slot* slots, int n, R
   }
 }
 
-cudaError_t launch_decide_local(Slot* slots, int n_slots, RankPartial* out, cudaStream_t s, const double* cta_sum,
-                                const uint32_t* cta_flag, const uint32_t* cta_grid) {
-  k_decide_local<<<1, kThreads, 0, s>>>(slots, n_slots, out, cta_sum, cta_flag, cta_grid);
+cudaError_t launch_decide_local(Slot* slots, int n_slots, RankPartial* out, cudaStream_t s, const double* slot_w,
+                                const double* cta_sum, const uint32_t* cta_flag, const uint32_t* cta_grid) {
+  k_decide_local<<<1, kThreads, 0, s>>>(slots, n_slots, out, slot_w, cta_sum, cta_flag, cta_grid);
+  return cudaGetLastError();
+}
+
+// sum of the data-parallel partials in rank order (the same order as k_decide_global)
+__global__ void k_combine_partials(const __grid_constant__ PartialPtrs pp, RankPartial* out) {
+  if (threadIdx.x != 0) return;
+  if (pp.wait_flags) wait_all(pp.wait_flags, pp.n, pp.epoch);
+  double sum = 0.0, flags = 0.0;
+  for (int r = 0; r < pp.n; ++r) {
+    sum += pp.p[r]->sumsq;
+    flags += pp.p[r]->flag;
+  }
+  out->sumsq = sum;
+  out->flag = flags;
+}
+cudaError_t launch_combine_partials(const PartialPtrs& pp, RankPartial* out, cudaStream_t s) {
+  k_combine_partials<<<1, 32, 0, s>>>(pp, out);
   return cudaGetLastError();
 }
 
 __global__ void k_decide_global(const __grid_constant__ PartialPtrs pp, DevState* st, const DecideParams p) {
   if (threadIdx.x != 0) return;
-  if (pp.wait_flags) wait_all(pp.wait_flags, p.n_ranks, pp.epoch);
+  if (pp.wait_flags) wait_all(pp.wait_flags, pp.n, pp.epoch);
   double sum = 0.0, flags = 0.0;
-  for (int r = 0; r < p.n_ranks; ++r) {
+  for (int r = 0; r < pp.n; ++r) {
     sum += pp.p[r]->sumsq;
     flags += pp.p[r]->flag;
   }

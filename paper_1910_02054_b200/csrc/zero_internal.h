@@ -160,11 +160,13 @@ cudaError_t launch_flatten_tma(const FlatArgs& a, int grid, cudaStream_t s, int 
 int flatten_tma_ctas_per_sm(int variant);
 cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s);
 // cta_*: optional per-CTA flatten partials (N_d == 1), slot i at [i * kMaxGrid, + cta_grid[i])
+// slot_w: optional per-slot norm weights (0 or 1; ZeRO x MP, R-MP1)
 cudaError_t launch_decide_local(Slot* slots, int n_slots, RankPartial* out, cudaStream_t s,
-                                const double* cta_sum = nullptr, const uint32_t* cta_flag = nullptr,
-                                const uint32_t* cta_grid = nullptr);
+                                const double* slot_w = nullptr, const double* cta_sum = nullptr,
+                                const uint32_t* cta_flag = nullptr, const uint32_t* cta_grid = nullptr);
 struct PartialPtrs {
   const RankPartial* p[kMaxRanks];
+  int n;                        // partials to sum, in order
   const uint64_t* wait_flags;   // cross-process PEER: wait until wait_flags[r] >= epoch
   uint64_t epoch;
 };
@@ -191,6 +193,8 @@ cudaError_t launch_wait(const WaitArgs& a, cudaStream_t s);
 cudaError_t launch_handshake(const SigArgs& a, const uint64_t* my_flags, uint64_t timeout_ns, uint32_t* result,
                              cudaStream_t s);
 cudaError_t launch_push_partial(const PushArgs& a, cudaStream_t s);
+// zero_step_begin: sum the partials of pp (waiting on its flags) into *out
+cudaError_t launch_combine_partials(const PartialPtrs& pp, RankPartial* out, cudaStream_t s);
 cudaError_t launch_decide_global(const PartialPtrs& partials, DevState* st, DecideParams p, cudaStream_t s);
 cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int variant);
 int adam_ctas_per_sm(int variant);

@@ -28,7 +28,7 @@ R16, R32 = 0, 1
 TRANSPORT = {"local": 0, "nccl": 1, "peer": 2}
 STATUS = {0: "ZERO_OK", 1: "ZERO_EINVAL", 2: "ZERO_ENOMEM", 3: "ZERO_ECUDA", 4: "ZERO_ENCCL",
           5: "ZERO_ESTATE", 6: "ZERO_EUNSUPPORTED"}
-Q_LAYOUT, Q_MEMORY, Q_COMM, Q_STEP, Q_BUCKETS, Q_PIECES, Q_STATE, Q_TIMING = range(8)
+Q_LAYOUT, Q_MEMORY, Q_COMM, Q_STEP, Q_BUCKETS, Q_PIECES, Q_STATE, Q_TIMING, Q_DECISION = range(9)
 
 
 class CTensor(C.Structure):
@@ -62,7 +62,8 @@ class CConfig(C.Structure):
                 ("param_dtype", C.c_int), ("grad_dtype", C.c_int), ("reduce_mode", C.c_int),
                 ("dynamic_loss_scale", C.c_int32), ("loss_scale", C.c_float), ("min_loss_scale", C.c_float),
                 ("scale_window", C.c_uint32), ("grad_prescale", C.c_float),
-                ("prefetch_depth", C.c_uint32), ("pool_buckets", C.c_uint32), ("timing", C.c_uint32)]
+                ("prefetch_depth", C.c_uint32), ("pool_buckets", C.c_uint32), ("timing", C.c_uint32),
+                ("mp_rank", C.c_uint32)]
 
 
 class CStepInfo(C.Structure):
@@ -100,7 +101,8 @@ class CDeviceState(C.Structure):
 
 EXPORTS = ["zero_plan_layout", "zero_init", "zero_buffer_sizes", "zero_bind_buffers", "zero_sim_group",
            "zero_peer_export", "zero_peer_open", "zero_export_state", "zero_import_state",
-           "zero_load_master", "zero_set_grad_ptrs", "zero_reduce_grads", "zero_step", "zero_gather_params",
+           "zero_load_master", "zero_set_grad_ptrs", "zero_reduce_grads", "zero_step", "zero_step_begin",
+           "zero_step_end", "zero_gather_params",
            "zero_release_params", "zero_param_view", "zero_query", "zero_last_error", "zero_destroy",
            "zero_model_state_bytes", "zero_comm_elems_per_rank", "zero_abi_version",
            "zero_pa_init", "zero_pa_get_info", "zero_pa_bind", "zero_pa_sim_group", "zero_pa_save",
@@ -130,6 +132,8 @@ def _load():
         "zero_set_grad_ptrs": ([P, C.POINTER(P)], C.c_int),
         "zero_reduce_grads": ([P, C.c_uint32, C.POINTER(P)], C.c_int),
         "zero_step": ([P, C.POINTER(CStepInfo)], C.c_int),
+        "zero_step_begin": ([P], C.c_int),
+        "zero_step_end": ([P, C.POINTER(CStepInfo)], C.c_int),
         "zero_gather_params": ([P, C.c_uint32, C.POINTER(P)], C.c_int),
         "zero_release_params": ([P, C.c_uint32], C.c_int),
         "zero_param_view": ([P, C.c_uint32, C.POINTER(P)], C.c_int),
@@ -201,6 +205,7 @@ class ZeroConfig:
     prefetch_depth: int = 1
     pool_buckets: int = 2
     timing: bool = False
+    mp_rank: int = 0          # ZeRO x MP: index in the model-parallel group (R-MP1)
 
     @staticmethod
     def defaults(param_dtype: str, **kw) -> "ZeroConfig":
@@ -217,7 +222,7 @@ class ZeroConfig:
                        _DT[self.param_dtype], _DT[self.grad_dtype], R32 if self.reduce_mode == "R32" else R16,
                        1 if self.dynamic_loss_scale else 0, self.loss_scale, self.min_loss_scale,
                        self.scale_window, self.grad_prescale, self.prefetch_depth, self.pool_buckets,
-                       1 if self.timing else 0)
+                       1 if self.timing else 0, self.mp_rank)
 
 
 def _desc(numels: Sequence[int], layers: Sequence[int], align: int, bucket_cap: int, flags=None):
@@ -368,6 +373,25 @@ class ZeroEngine:
         """Enqueue zero_step; the record lands in pinned memory (read with step_info())."""
         p = C.cast(C.c_void_p(self._info_host.data_ptr()), C.POINTER(CStepInfo))
         _check(lib.zero_step(self._ctx, p), self._ctx)
+
+    def step_begin(self):
+        """zero_step_begin (ZeRO x MP): the step up to the decision; the DP-combined
+        partial is then in decision_partial()."""
+        _check(lib.zero_step_begin(self._ctx), self._ctx)
+
+    def step_end(self):
+        """zero_step_end: decide from the (MP-all-reduced) partial and finish the step."""
+        p = C.cast(C.c_void_p(self._info_host.data_ptr()), C.POINTER(CStepInfo))
+        _check(lib.zero_step_end(self._ctx, p), self._ctx)
+
+    def decision_partial(self) -> torch.Tensor:
+        """float64[2] view {sum of squares, overflow count} of the partial zero_step_begin
+        writes: SUM-all-reduce it over the MP group between step_begin and step_end."""
+        ptr = C.c_void_p()
+        _check(lib.zero_query(self._ctx, Q_DECISION, C.byref(ptr), C.sizeof(ptr)), self._ctx)
+        scratch = self.arenas["scratch"]
+        off = ptr.value - scratch.data_ptr()
+        return scratch[off:off + 16].view(torch.float64)
 
     def step_info(self) -> CStepInfo:
         """The last step's record (synchronizes the device)."""

@@ -150,6 +150,54 @@ def gpt_layout(n_layer: int, h: int, vocab: int, seq: int) -> List[TensorSpec]:
     return out
 
 
+def gpt_mp_layout(n_layer: int, h: int, vocab: int, seq: int, n_m: int):
+    """The GPT-style model of gpt_layout under Megatron tensor slicing over n_m MP ranks
+    (the MP the paper composes ZeRO with): qkv / fc are column-parallel
+    (weights and biases split), proj / fc2 row-parallel (weights split, biases
+    replicated), the embedding vocabulary-parallel, wpe and every LayerNorm replicated.
+
+    Returns (U, per_rank): U is the union tensor list (each replicated tensor once,
+    each split tensor's n_m parts), per_rank[j] = (tensors, flags, index into U) for MP
+    rank j in forward order; flags[t] = 1 for a replicated tensor.  Shapes only."""
+    assert h % n_m == 0
+    U: List[TensorSpec] = []
+    per = [([], [], []) for _ in range(n_m)]
+
+    def rep(name, numel, layer, role=ROLE_WEIGHT):
+        U.append(TensorSpec(name, numel, layer, role))
+        for j in range(n_m):
+            per[j][0].append(U[-1])
+            per[j][1].append(1)
+            per[j][2].append(len(U) - 1)
+
+    def split(name, numels, layer, role=ROLE_WEIGHT):
+        for j in range(n_m):
+            U.append(TensorSpec(f"{name}@{j}", numels[j], layer, role))
+            per[j][0].append(U[-1])
+            per[j][1].append(0)
+            per[j][2].append(len(U) - 1)
+
+    split("wte", [(vocab // n_m + (j < vocab % n_m)) * h for j in range(n_m)], 0)
+    rep("wpe", seq * h, 0)
+    for b in range(n_layer):
+        L, p, q = b + 1, f"h{b}.", h // n_m
+        rep(p + "ln1.w", h, L, ROLE_LNW)
+        rep(p + "ln1.b", h, L, ROLE_BIAS)
+        split(p + "qkv.W", [h * 3 * q] * n_m, L)
+        split(p + "qkv.b", [3 * q] * n_m, L, ROLE_BIAS)
+        split(p + "proj.W", [q * h] * n_m, L)
+        rep(p + "proj.b", h, L, ROLE_BIAS)
+        rep(p + "ln2.w", h, L, ROLE_LNW)
+        rep(p + "ln2.b", h, L, ROLE_BIAS)
+        split(p + "fc.W", [h * 4 * q] * n_m, L)
+        split(p + "fc.b", [4 * q] * n_m, L, ROLE_BIAS)
+        split(p + "fc2.W", [4 * q * h] * n_m, L)
+        rep(p + "fc2.b", h, L, ROLE_BIAS)
+    rep("lnf.w", h, n_layer + 1, ROLE_LNW)
+    rep("lnf.b", h, n_layer + 1, ROLE_BIAS)
+    return U, per
+
+
 def gpt2_1p5b() -> List[TensorSpec]:
     """Config 2: 48 x 1600, V=50257, S=1024 -> Psi = 1,557,611,200."""
     return gpt_layout(48, 1600, 50257, 1024)

@@ -173,3 +173,33 @@ def test_layout_mp_groups_match_oracle(z):
         a = rnd.choice([1, 8, 64])
         cb = rnd.choice([0, n * a, rnd.randint(n * a, 20 * n * a)])
         _cmp_layout(z, numels, layers, n, a, cb, groups)
+
+
+@pytest.mark.parametrize("stage", [1, 2, 3])
+def test_mp_composition_memory(z, stage):
+    """ZeRO x MP (memory reduced by N_d x N_m): each rank of a 4-way Megatron
+    split of GPT-2 1.5B (synth.gpt_mp_layout) running ZeRO over N_d = 8 holds exactly
+    the stage formula of its own padded slice, and about a quarter of the unsplit
+    model's per-rank model states (the excess is the replicated LayerNorm / bias /
+    position-embedding tensors, 0.3 % of Psi)."""
+    from paper_1910_02054_b200.zero import ZeroEngine
+    n_d, n_m = 8, 4
+    U, per = synth.gpt_mp_layout(48, 1600, 50257, 1024, n_m)
+    full = synth.gpt2_1p5b()
+    e1 = ZeroEngine([t.numel for t in full], [t.layer for t in full], n_d, 0, stage, transport="peer", bind=False)
+    m1 = e1.memory()
+    base = m1.params16 + m1.grads16 + m1.optimizer
+    tot = 0
+    for j in range(n_m):
+        ts, flags, _ = per[j]
+        e = ZeroEngine([t.numel for t in ts], [t.layer for t in ts], n_d, 0, stage, transport="peer", bind=False,
+                       flags=flags)
+        m = e.memory()
+        got = m.params16 + m.grads16 + m.optimizer
+        assert got == P.model_state_bytes(e.info.psi_padded, 12, n_d, stage)
+        assert abs(got / base - 1 / n_m) < 0.01
+        tot += got
+        e.destroy()
+    rep = sum(t.numel for t, f in zip(per[0][0], per[0][1]) if f)
+    assert rep / synth.psi(U) < 0.004
+    e1.destroy()
