@@ -27,7 +27,7 @@ from typing import Callable, Dict, List, Optional, Sequence, Tuple
 
 import torch
 
-from .zero import ZeroConfig, ZeroEngine
+from .zero import MP_REPLICATED, ZeroConfig, ZeroEngine
 
 _DT = {torch.bfloat16: "bf16", torch.float16: "fp16"}
 
@@ -58,7 +58,12 @@ class ZeroOptimizer:
                  n_d: int = 1, rank: int = 0, transport: str = "local", nccl_comm: int = 0,
                  layer_of: Optional[Callable[[Sequence[str]], List[int]]] = None,
                  bucket_cap: int = 1 << 26, align: int = 64, stream: Optional[torch.cuda.Stream] = None,
-                 engine_factory=None, process_group=None):
+                 engine_factory=None, process_group=None, mp_group=None,
+                 mp_replicated: Optional[Callable[[Sequence[str]], List[bool]]] = None):
+        """mp_group (ZeRO x MP): the torch.distributed group of this rank's model-
+        parallel peers; the step decision is then all-reduced over it (zero_step_begin /
+        zero_step_end) and mp_replicated(names) marks the tensors every MP rank holds
+        (their gradient norm counts once, reading R-MP1)."""
         if stage not in (0, 1, 2, 3):
             raise ValueError("stage must be 0..3")
         named = [(n, p) for n, p in model.named_parameters() if p.requires_grad]
@@ -75,11 +80,20 @@ class ZeroOptimizer:
         self.params = [p for _, p in named]
         layers = (layer_of or default_layer_of)(self.names)
         self.stage = stage
+        self.mp_group = mp_group
+        flags = None
+        if mp_group is not None:
+            import dataclasses
+            import torch.distributed as dist
+            self.config = dataclasses.replace(self.config, mp_rank=dist.get_rank(mp_group))
+            if mp_replicated is not None:
+                flags = [MP_REPLICATED if f else 0 for f in mp_replicated(self.names)]
         if engine_factory is not None:          # e.g. one rank of a ZeroSimGroup
             self.engine = engine_factory([p.numel() for p in self.params], layers)
         else:
             self.engine = ZeroEngine([p.numel() for p in self.params], layers, n_d, rank, stage, self.config,
-                                     transport, nccl_comm, stream, align, bucket_cap, self.params[0].device)
+                                     transport, nccl_comm, stream, align, bucket_cap, self.params[0].device,
+                                     flags=flags)
             if transport == "peer" and n_d > 1:   # one process per rank: open the CUDA-IPC peer table
                 self.engine.link_peers(process_group)
         self.shapes = [p.shape for p in self.params]
@@ -169,7 +183,13 @@ class ZeroOptimizer:
         missing = [k for k, r in enumerate(self._remaining) if r != 0]
         if missing:
             raise RuntimeError(f"buckets {missing[:8]} were not fully produced by backward")
-        self.engine.step()
+        if self.mp_group is not None:    # the decision spans the MP group (16-byte all-reduce)
+            import torch.distributed as dist
+            self.engine.step_begin()
+            dist.all_reduce(self.engine.decision_partial(), group=self.mp_group)
+            self.engine.step_end()
+        else:
+            self.engine.step()
         self._remaining = [len(ts) for ts in self._bucket_tensors]
         self._ptrs = [None] * len(self.params)
         self.reduced_order = []

@@ -138,3 +138,95 @@ def test_step_begin_end_equals_step():
     with pytest.raises(Exception, match="ESTATE"):
         p.engines[0].step_end()
     p.destroy()
+
+
+def _mp_torch_worker(j, port, q):
+    import os
+    import sys
+    import traceback
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "tests")]
+    try:
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        from harness import bits16
+        from oracle import step as OS
+        from paper_1910_02054_b200 import ZeroConfig
+        from paper_1910_02054_b200.torch_zero import ZeroOptimizer
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=j, world_size=2)
+        torch.cuda.set_device(0)
+        h, k = 96, 40
+
+        class Slice(torch.nn.Module):         # a replicated LayerNorm weight + this rank's weight slice
+            def __init__(self):
+                super().__init__()
+                torch.manual_seed(11)
+                self.ln = torch.nn.Parameter(torch.randn(h).to(torch.bfloat16))
+                torch.manual_seed(20 + j)
+                self.w = torch.nn.Parameter(torch.randn(h * k).mul(0.02).to(torch.bfloat16))
+
+        model = Slice().cuda()
+        init = {}
+        torch.manual_seed(11)
+        init["ln"] = torch.randn(h).to(torch.bfloat16).float().numpy()
+        for jj in range(2):
+            torch.manual_seed(20 + jj)
+            init[jj] = torch.randn(h * k).mul(0.02).to(torch.bfloat16).float().numpy()
+        cfg = OS.AdamConfig.defaults("bf16", max_grad_norm=0.5)
+        zc = ZeroConfig.defaults("bf16", max_grad_norm=0.5)
+        opt = ZeroOptimizer(model, stage=1, config=zc, mp_group=dist.group.WORLD,
+                            mp_replicated=lambda names: [n == "ln" for n in names])
+        ost = OS.init_state([init["ln"], init[0], init[1]], cfg)
+        for s in range(4):
+            gen = torch.Generator().manual_seed(1000 + s)
+            c_ln = torch.randn(h, generator=gen).to(torch.bfloat16)
+            c_w = [torch.randn(h * k, generator=gen).to(torch.bfloat16) for _ in range(2)]
+            if s == 2:
+                c_w[1][7] = float("inf")     # overflow on MP rank 1 only: both must skip
+            loss = (model.ln.float() * c_ln.cuda().float()).sum() + (model.w.float() * c_w[j].cuda().float()).sum()
+            loss.backward()
+            opt.step()
+            OS.step(ost, [[c_ln.float(), c_w[0].float(), c_w[1].float()]], cfg)
+        torch.cuda.synchronize()
+        info = opt.step_info()
+        assert info.t == 3, info.t               # 4 steps, one skipped everywhere
+        assert np.array_equal(bits16(model.ln.detach()), ost.p16[0]), "ln"
+        assert np.array_equal(bits16(model.w.detach()), ost.p16[1 + j]), "w"
+        dist.barrier()
+        opt.close()
+        dist.destroy_process_group()
+        q.put("ok")
+    except Exception:
+        q.put(traceback.format_exc())
+        raise
+
+
+def test_zero_optimizer_mp_group_two_processes():
+    """ZeroOptimizer(mp_group=...): two MP ranks in two processes, each with a replicated
+    tensor and its own slice; the decision is all-reduced over the MP group (gloo), so
+    both clip by the union model's norm (replicated counted once) and both skip the
+    step in which only MP rank 1 overflowed -- bit-exact vs the union oracle."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_mp_torch_worker, args=(j, port, q)) for j in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+    hung = [p for p in procs if p.is_alive()]
+    for p in hung:
+        p.kill()
+        p.join(10)
+    msgs = []
+    while not q.empty():
+        msgs.append(q.get())
+    assert not hung, f"workers hung: {msgs}"
+    assert msgs == ["ok", "ok"], msgs
