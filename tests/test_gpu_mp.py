@@ -188,7 +188,7 @@ def _mp_torch_worker(j, port, q):
             loss = (model.ln.float() * c_ln.cuda().float()).sum() + (model.w.float() * c_w[j].cuda().float()).sum()
             loss.backward()
             opt.step()
-            OS.step(ost, [[c_ln.float(), c_w[0].float(), c_w[1].float()]], cfg)
+            OS.step(ost, [OS.grads_from_torch([c_ln, c_w[0], c_w[1]])], cfg)
         torch.cuda.synchronize()
         info = opt.step_info()
         assert info.t == 3, info.t               # 4 steps, one skipped everywhere
