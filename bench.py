@@ -494,7 +494,9 @@ def main():
         h2d_ms = h0.elapsed_time(h1)
         barrier()
         K = args.e2e_steps
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
+        e0.record(copy_stream)
         with torch.cuda.stream(copy_stream):
             bufs[0].copy_(host, non_blocking=True)
             copied[0].record(copy_stream)
@@ -514,16 +516,20 @@ def main():
                     copied[nxt].record(copy_stream)
             stream.synchronize()                    # the host reads step s's result
             _ = bytes(rec.numpy()[:32])
+        e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / K, dev)
+        e2e_dev_ms = max_over_ranks(e0.elapsed_time(e1) / K, dev)
         eng.set_grads(grads)
         line["e2e"] = {"value": psi_total / (e2e_ms * 1e-3) / 1e9, "unit": "Gparams/s",
                        "h2d_bytes_per_step": int(grad_buf.numel() * grad_buf.element_size()),
                        "d2h_bytes_per_step": 32, "ms_per_step": e2e_ms, "steps": K,
+                       "device_ms_per_step": e2e_dev_ms,
                        "h2d_alone_ms": h2d_ms,
                        "h2d_gbs": grad_buf.numel() * grad_buf.element_size() / (h2d_ms * 1e-3) / 1e9,
                        "frac_of_h2d_bound": max(h2d_ms, ms) / e2e_ms,
-                       "note": "host wall clock; H2D of step s+1 overlaps step s (double-buffered)"}
+                       "note": "value from the host wall clock (device_ms_per_step: CUDA events from the first H2D "
+                               "to the last step's end); H2D of step s+1 overlaps step s (double-buffered)"}
 
     if rank == 0 and not args.no_cpu_baseline:
         v, desc, n, dt = oracle_sample_run(tensors, args.dtype, args.seed, 2, 0, args.cpu_budget_s)
