@@ -2,9 +2,18 @@
 
 The partitioned mixed-precision Adam step (stages P_os, P_os+g, P_os+g+p) runs in
 hand-written sm_100a kernels behind include/zero_b200.h; see DESIGN.md.
-"""
-from .zero import (ZeroConfig, ZeroEngine, ZeroError, ZeroSimGroup, comm_elems_per_rank,  # noqa: F401
-                   consolidate_states, model_state_bytes, nccl_comm_ptr, plan_layout)
 
+The names below are resolved on first use, which loads libzero_b200.so and raises
+ImportError if it has not been built (there is no CPU fallback); importing the
+package alone does not load it, so `python -m paper_1910_02054_b200._build` works
+in a fresh checkout.
+"""
 __all__ = ["ZeroConfig", "ZeroEngine", "ZeroError", "ZeroSimGroup", "plan_layout", "model_state_bytes",
            "comm_elems_per_rank", "nccl_comm_ptr", "consolidate_states"]
+
+
+def __getattr__(name):
+    if name in __all__:
+        from . import zero
+        return getattr(zero, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

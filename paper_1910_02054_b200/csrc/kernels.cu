@@ -309,17 +309,42 @@ struct SrcLoad<DT_F32> {
 // (data pieces and zero pieces for alignment gaps / padding).  CTA b handles the
 // contiguous slice [b*per_cta, (b+1)*per_cta) of that range, walking the pieces it
 // overlaps; each thread keeps V 128-bit loads in flight.
-template <int SDT, int DDT, bool kCopy, int V>
-__global__ void __launch_bounds__(kThreads, 6) k_flatten(const __grid_constant__ FlatArgs a) {  // <= 40 regs: +1 % (A/B)
+// the N_d = 1 epilogue of one flattened 16-bit value b (reading c-4 / P:282):
+//  kEpi 0: none; 1: u = fp32(b * inv), sum += u^2 (fp64), flag |= !finite(b);
+//  2: inv is a power of two <= 1 (the usual case: 1/(S*sigma)), so u^2 = b^2 * inv^2 exactly
+//     and the kernel scales the sum once; b^2 is formed from b's bits (normal numbers)
+//     with integer ops, and the flag is read off the sum (finite iff every b is).
+template <int DDT, int kEpi>
+__device__ __forceinline__ void epi_elem(uint32_t b, float inv, double& sumsq, uint32_t& flag) {
+  using D = H16<DDT>;
+  if (kEpi == 1) {
+    flag |= D::nonfinite(b);
+    sq_acc(sumsq, __fmul_rn(D::widen(b), inv));
+  } else if (kEpi == 2) {
+    const uint32_t x = b & 0x7FFFu;
+    constexpr uint32_t kMinNormal = DDT == DT_BF16 ? 0x0080u : 0x0400u;
+    constexpr uint32_t kSpan = DDT == DT_BF16 ? 0x7F00u : 0x7800u;   // [min normal, inf)
+    if (x - kMinNormal < kSpan) {   // rebias the exponent into fp64 (bias 1023)
+      const uint32_t hi = DDT == DT_BF16 ? (x << 13) + (896u << 20) : (x << 10) + (1008u << 20);
+      const double d = __hiloint2double((int)hi, 0);
+      sumsq = fma(d, d, sumsq);
+    } else if (x != 0) {           // subnormal, inf, nan
+      const double d = f32_to_f64_slow(D::widen(b));
+      sumsq = fma(d, d, sumsq);
+    }
+  }
+}
+
+__device__ __forceinline__ bool pow2_at_most_one(float inv) {
+  const uint32_t u = __float_as_uint(inv);
+  return (u & 0x807FFFFFu) == 0u && u != 0u && inv <= 1.0f;   // +2^k, k <= 0, normal
+}
+
+template <int SDT, int DDT, bool kCopy, int V, int kEpi>
+__device__ __forceinline__ void flatten_body(const FlatArgs& a, float inv, double& sumsq, uint32_t& flag) {
   using S = SrcLoad<SDT>;
   using D = H16<DDT>;
-  // PDL: the next bucket's flatten (independent data) may start as soon as every CTA
-  // of this one is resident; a no-op without a programmatic dependent
-  asm volatile("griddepcontrol.launch_dependents;");
   const float sigma = a.sigma;
-  const float inv = a.epilogue ? a.st->inv_cur : 0.0f;
-  double sumsq = 0.0;
-  uint32_t flag = 0;
   uint16_t* dst_base = reinterpret_cast<uint16_t*>(a.dst);
   const uint64_t r0 = a.pieces[0].dst_off;
   const uint64_t r1 = a.pieces[a.n_pieces - 1].dst_off + a.pieces[a.n_pieces - 1].count;
@@ -351,11 +376,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_flatten(const __grid_constant__
       const float xv = S::one(src, j);
       const uint32_t b = kCopy ? D::narrow(xv) : D::narrow(__fmul_rn(xv, sigma));
       dst[j] = (uint16_t)b;
-      if (a.epilogue) {
-        flag |= D::nonfinite(b);
-        const float u = __fmul_rn(D::widen(b), inv);
-        sq_acc(sumsq, u);
-      }
+      epi_elem<DDT, kEpi>(b, inv, sumsq, flag);
     };
     auto emit8 = [&](uint32_t i, const float* x) {
       U4 o;
@@ -363,11 +384,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_flatten(const __grid_constant__
       for (int j = 0; j < 8; ++j) {
         const uint32_t b = kCopy ? D::narrow(x[j]) : D::narrow(__fmul_rn(x[j], sigma));
         h_set(o, j, b);
-        if (a.epilogue) {
-          flag |= D::nonfinite(b);
-          const float u = __fmul_rn(D::widen(b), inv);
-          sq_acc(sumsq, u);
-        }
+        epi_elem<DDT, kEpi>(b, inv, sumsq, flag);
       }
       st128(dst + i, o);
     };
@@ -386,13 +403,9 @@ __global__ void __launch_bounds__(kThreads, 6) k_flatten(const __grid_constant__
           const uint32_t i = i0 + u * kThreads * 8;
           if (u == 0 || i < nv) {
             st128(dst + i, r[u]);
-            if (a.epilogue) {
+            if (kEpi) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const uint32_t b = h_get(r[u], j);
-                flag |= D::nonfinite(b);
-                sq_acc(sumsq, __fmul_rn(D::widen(b), inv));
-              }
+              for (int j = 0; j < 8; ++j) epi_elem<DDT, kEpi>(h_get(r[u], j), inv, sumsq, flag);
             }
           }
         }
@@ -420,7 +433,28 @@ __global__ void __launch_bounds__(kThreads, 6) k_flatten(const __grid_constant__
     }
     cur = pend;
   }
-  if (a.epilogue) flat_publish(a, sumsq, flag);
+}
+
+template <int SDT, int DDT, bool kCopy, int V>
+__global__ void __launch_bounds__(kThreads, 6) k_flatten(const __grid_constant__ FlatArgs a) {  // <= 40 regs: +1 % (A/B)
+  // PDL: the next bucket's flatten (independent data) may start as soon as every CTA
+  // of this one is resident; a no-op without a programmatic dependent
+  asm volatile("griddepcontrol.launch_dependents;");
+  double sumsq = 0.0;
+  uint32_t flag = 0;
+  if (!a.epilogue) {
+    flatten_body<SDT, DDT, kCopy, V, 0>(a, 0.0f, sumsq, flag);
+  } else {
+    const float inv = a.st->inv_cur;
+    if (pow2_at_most_one(inv)) {
+      flatten_body<SDT, DDT, kCopy, V, 2>(a, inv, sumsq, flag);
+      flag = isfinite(sumsq) ? 0u : 1u;          // b^2 of a finite 16-bit value is finite in fp64
+      sumsq *= (double)inv * (double)inv;        // exact: a power of two, no under/overflow
+    } else {
+      flatten_body<SDT, DDT, kCopy, V, 1>(a, inv, sumsq, flag);
+    }
+    flat_publish(a, sumsq, flag);
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: complete only after the previous flatten
 }
 
