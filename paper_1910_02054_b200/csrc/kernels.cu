@@ -1028,7 +1028,7 @@ cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s) {
 // slots (ascending bucket, fixed tree) into one RankPartial; decide_global folds
 // the ranks' partials in ascending rank and advances the loss-scale machine.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_decide_local(Slot* slots, int n, RankPartial* out, const double* slot_w,
+__global__ void __launch_bounds__(1024) k_decide_local(Slot* slots, int n, RankPartial* out, const double* slot_w,
                                                            const double* cta_sum, const uint32_t* cta_flag,
                                                            const uint32_t* cta_grid) {
   if (cta_sum) {  // N_d = 1: combine each slot's per-CTA flatten partials (warp per slot, fixed order)
@@ -1039,7 +1039,8 @@ __global__ void __launch_bounds__(kThreads) k_decide_local(Slot* slots, int n, R
       const uint32_t* cf = cta_flag + (size_t)i * kMaxGrid;
       double s = 0.0;
       uint32_t f = 0;
-      for (uint32_t c = lane; c < g; c += 32) {
+#pragma unroll 4
+      for (uint32_t c = lane; c < g; c += 32) {   // loads pipelined, sums in CTA order
         s += cs[c];
         f |= cf[c];
       }
@@ -1067,7 +1068,8 @@ __global__ void __launch_bounds__(kThreads) k_decide_local(Slot* slots, int n, R
 
 cudaError_t launch_decide_local(Slot* slots, int n_slots, RankPartial* out, cudaStream_t s, const double* slot_w,
                                 const double* cta_sum, const uint32_t* cta_flag, const uint32_t* cta_grid) {
-  k_decide_local<<<1, kThreads, 0, s>>>(slots, n_slots, out, slot_w, cta_sum, cta_flag, cta_grid);
+  // 32 warps: one per bucket slot at a time for the N_d = 1 per-CTA partials
+  k_decide_local<<<1, cta_sum ? 1024 : kThreads, 0, s>>>(slots, n_slots, out, slot_w, cta_sum, cta_flag, cta_grid);
   return cudaGetLastError();
 }
 
