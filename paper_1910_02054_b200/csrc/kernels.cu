@@ -323,15 +323,16 @@ __device__ __forceinline__ void epi_elem(uint32_t b, float inv, double& sumsq, u
   } else if (kEpi == 2) {
     const uint32_t x = b & 0x7FFFu;
     constexpr uint32_t kMinNormal = DDT == DT_BF16 ? 0x0080u : 0x0400u;
-    constexpr uint32_t kSpan = DDT == DT_BF16 ? 0x7F00u : 0x7800u;   // [min normal, inf)
-    if (x - kMinNormal < kSpan) {   // rebias the exponent into fp64 (bias 1023)
-      const uint32_t hi = DDT == DT_BF16 ? (x << 13) + (896u << 20) : (x << 10) + (1008u << 20);
-      const double d = __hiloint2double((int)hi, 0);
-      sumsq = fma(d, d, sumsq);
-    } else if (x != 0) {           // subnormal, inf, nan
-      const double d = f32_to_f64_slow(D::widen(b));
-      sumsq = fma(d, d, sumsq);
-    }
+    constexpr uint32_t kInf = DDT == DT_BF16 ? 0x7F80u : 0x7C00u;
+    constexpr double kMinNormalValue = DDT == DT_BF16 ? 0x1p-126 : 0x1p-14;
+    // rebias the exponent into fp64 (bias 1023): exact for normal numbers
+    const uint32_t hi = DDT == DT_BF16 ? (x << 13) + (896u << 20) : (x << 10) + (1008u << 20);
+    const double r = __hiloint2double((int)hi, 0);
+    double d;
+    if (x - kMinNormal < kInf - kMinNormal) d = r;
+    else if (x < kMinNormal) d = fma(2.0, r, -kMinNormalValue);   // zero / subnormal: 2r - min = m * 2^-(bias+mant-1), exact
+    else d = f32_to_f64_slow(D::widen(b));                         // inf / nan
+    sumsq = fma(d, d, sumsq);
   }
 }
 
