@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define ZERO_ABI_VERSION 1
+#define ZERO_ABI_VERSION 2     /* 2: zero_config.mp_rank, zero_tensor.flags, zero_step_begin/end, zero_pa_* */
 #define ZERO_MAX_RANKS 8      /* one NVL8 box */
 
 typedef enum {

@@ -22,6 +22,7 @@ _LIB_PATH = os.environ.get("ZERO_LIB_PATH") or os.path.join(_PKG, "libzero_b200.
 # ---------------------------------------------------------------------------
 # ABI structs (mirror include/zero_b200.h field by field)
 # ---------------------------------------------------------------------------
+ABI_VERSION = 2           # include/zero_b200.h ZERO_ABI_VERSION
 FP16, BF16, FP32 = 0, 1, 2
 MP_REPLICATED = 1          # zero_tensor.flags: replicated across the MP group (reading R-MP1)
 R16, R32 = 0, 1
@@ -161,6 +162,8 @@ def _load():
         f = getattr(lib, name)
         f.argtypes = args
         f.restype = res
+    if lib.zero_abi_version() != ABI_VERSION:   # the ctypes structs below mirror this ABI
+        raise ImportError(f"{_LIB_PATH} has ABI {lib.zero_abi_version()}, the binding expects {ABI_VERSION}: rebuild")
     return lib
 
 
