@@ -328,11 +328,19 @@ __device__ __forceinline__ void epi_elem(uint32_t b, float inv, double& sumsq, u
     // rebias the exponent into fp64 (bias 1023): exact for normal numbers
     const uint32_t hi = DDT == DT_BF16 ? (x << 13) + (896u << 20) : (x << 10) + (1008u << 20);
     const double r = __hiloint2double((int)hi, 0);
-    double d;
-    if (x - kMinNormal < kInf - kMinNormal) d = r;
-    else if (x < kMinNormal) d = fma(2.0, r, -kMinNormalValue);   // zero / subnormal: 2r - min = m * 2^-(bias+mant-1), exact
-    else d = f32_to_f64_slow(D::widen(b));                         // inf / nan
-    sumsq = fma(d, d, sumsq);
+    if (DDT == DT_BF16) {   // bf16 subnormals (< 2^-126) do not occur in practice: branch, not predicate
+      if (x - kMinNormal < kInf - kMinNormal) sumsq = fma(r, r, sumsq);
+      else if (x != 0) {
+        const double d = f32_to_f64_slow(D::widen(b));           // subnormal, inf, nan
+        sumsq = fma(d, d, sumsq);
+      }
+    } else {                // fp16 subnormals are common (|g| < 2^-14): handled inline, exactly
+      double d;
+      if (x - kMinNormal < kInf - kMinNormal) d = r;
+      else if (x < kMinNormal) d = fma(2.0, r, -kMinNormalValue);   // zero / subnormal: 2r - min = m * 2^-24, exact
+      else d = f32_to_f64_slow(D::widen(b));                         // inf / nan
+      sumsq = fma(d, d, sumsq);
+    }
   }
 }
 
