@@ -855,7 +855,30 @@ int flatten_tma_ctas_per_sm(int) { return 1; }
 // NR: number of ranks known at compile time (2, 4, 8; 0 = a.n at run time).  U: 8-element
 // groups per thread per iteration, so that U*NR 128-bit loads are in flight before the
 // sums (NVLink latency is ~2 us: the pull needs many bytes in flight per SM).
-template <int DT, bool kR32>
+// epilogue of one reduced value (as epi_elem): kEpi 1 = u = fp32(G * inv), flag per element;
+// kEpi 2 = inv a power of two <= 1: sum G^2 (R32) or b^2 from the bits (R16), scaled and
+// flagged once at the end of the kernel
+template <int DT, bool kR32, int kEpi>
+__device__ __forceinline__ void rs_epi(float G32, uint32_t b16, float inv, double& sumsq, uint32_t& flag) {
+  using D = H16<DT>;
+  if (kR32) {
+    if (kEpi == 1) {
+      flag |= (uint32_t)!isfinite(G32);
+      sq_acc(sumsq, __fmul_rn(G32, inv));
+    } else {
+      sq_acc(sumsq, G32);
+    }
+  } else {
+    if (kEpi == 1) {
+      flag |= D::nonfinite(b16);
+      sq_acc(sumsq, __fmul_rn(D::widen(b16), inv));
+    } else {
+      epi_elem<DT, 2>(b16, inv, sumsq, flag);
+    }
+  }
+}
+
+template <int DT, bool kR32, int kEpi>
 __device__ __forceinline__ void rs_emit8(const RSArgs& a, uint64_t i, const float (&acc)[8], bool store, float inv,
                                          double& sumsq, uint32_t& flag) {
   using D = H16<DT>;
@@ -864,8 +887,7 @@ __device__ __forceinline__ void rs_emit8(const RSArgs& a, uint64_t i, const floa
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       o.x[j] = __float_as_uint(acc[j]);
-      flag |= (uint32_t)!isfinite(acc[j]);
-      sq_acc(sumsq, __fmul_rn(acc[j], inv));
+      rs_epi<DT, true, kEpi>(acc[j], 0u, inv, sumsq, flag);
     }
     if (store) st256(reinterpret_cast<float*>(a.dst) + i, o);
   } else {
@@ -874,25 +896,17 @@ __device__ __forceinline__ void rs_emit8(const RSArgs& a, uint64_t i, const floa
     for (int j = 0; j < 8; ++j) {
       const uint32_t b = D::narrow(acc[j]);
       h_set(o, j, b);
-      flag |= D::nonfinite(b);
-      sq_acc(sumsq, __fmul_rn(D::widen(b), inv));
+      rs_epi<DT, false, kEpi>(0.0f, b, inv, sumsq, flag);
     }
     if (store) st128(reinterpret_cast<uint16_t*>(a.dst) + i, o);
   }
 }
 
-template <int DT, bool kR32, bool kReduce, bool kVec, int NR, int U>
-__global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_constant__ RSArgs a) {
+template <int DT, bool kR32, bool kReduce, bool kVec, int NR, int U, int kEpi>
+__device__ __forceinline__ void rs_body(const RSArgs& a, float inv, double& sumsq, uint32_t& flag) {
   using D = H16<DT>;
   constexpr int R = NR > 0 ? NR : kMaxRanks;
   const int n = NR > 0 ? NR : a.n;
-  if (a.wait_flags) {  // every rank has flattened this bucket (cross-process PEER)
-    if (threadIdx.x == 0) wait_all(a.wait_flags, a.n, a.epoch);
-    __syncthreads();
-  }
-  const float inv = a.st->inv_cur;
-  double sumsq = 0.0;
-  uint32_t flag = 0;
   const uint64_t step = (uint64_t)kThreads * (kVec ? 8 : 1);
   const uint64_t stride = (uint64_t)gridDim.x * step * (kVec ? U : 1);
   for (uint64_t i0 = ((uint64_t)blockIdx.x * kThreads * (kVec ? U : 1) + threadIdx.x) * (kVec ? 8 : 1); i0 < a.count;
@@ -922,20 +936,18 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
 #pragma unroll
                 for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], D::widen(h_get(v[u][r], j)));
               }
-            rs_emit8<DT, kR32>(a, i, acc, true, inv, sumsq, flag);
+            rs_emit8<DT, kR32, kEpi>(a, i, acc, true, inv, sumsq, flag);
           } else if (i < a.count) {
             for (uint64_t k = i; k < a.count; ++k) {   // ragged tail of the second group
               float acc = D::widen(reinterpret_cast<const uint16_t*>(a.src[0])[k]);
               for (int r = 1; r < n; ++r) acc = __fadd_rn(acc, D::widen(reinterpret_cast<const uint16_t*>(a.src[r])[k]));
               if (kR32) {
-                flag |= (uint32_t)!isfinite(acc);
                 reinterpret_cast<float*>(a.dst)[k] = acc;
-                sq_acc(sumsq, __fmul_rn(acc, inv));
+                rs_epi<DT, true, kEpi>(acc, 0u, inv, sumsq, flag);
               } else {
                 const uint32_t b = D::narrow(acc);
-                flag |= D::nonfinite(b);
                 reinterpret_cast<uint16_t*>(a.dst)[k] = (uint16_t)b;
-                sq_acc(sumsq, __fmul_rn(D::widen(b), inv));
+                rs_epi<DT, false, kEpi>(0.0f, b, inv, sumsq, flag);
               }
             }
           }
@@ -946,16 +958,8 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
           const uint64_t i = i0 + (uint64_t)u * step;
           if (!(u == 0 || i + 8 <= a.count)) {
             for (uint64_t k = i; k < a.count; ++k) {
-              float G;
-              if (kR32) {
-                G = reinterpret_cast<const float*>(a.dst)[k];
-                flag |= (uint32_t)!isfinite(G);
-              } else {
-                const uint32_t b = reinterpret_cast<const uint16_t*>(a.dst)[k];
-                flag |= D::nonfinite(b);
-                G = D::widen(b);
-              }
-              sq_acc(sumsq, __fmul_rn(G, inv));
+              if (kR32) rs_epi<DT, true, kEpi>(reinterpret_cast<const float*>(a.dst)[k], 0u, inv, sumsq, flag);
+              else rs_epi<DT, false, kEpi>(0.0f, reinterpret_cast<const uint16_t*>(a.dst)[k], inv, sumsq, flag);
             }
             continue;
           }
@@ -969,7 +973,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[j] = D::widen(h_get(w, j));
           }
-          rs_emit8<DT, kR32>(a, i, acc, false, inv, sumsq, flag);
+          rs_emit8<DT, kR32, kEpi>(a, i, acc, false, inv, sumsq, flag);
         }
       }
     } else {
@@ -984,20 +988,34 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
         } else {
           acc = D::widen(reinterpret_cast<const uint16_t*>(a.dst)[k]);
         }
-        float G;
         if (kR32) {
-          G = acc;
-          flag |= (uint32_t)!isfinite(acc);
           if (kReduce) reinterpret_cast<float*>(a.dst)[k] = acc;
+          rs_epi<DT, true, kEpi>(acc, 0u, inv, sumsq, flag);
         } else {
           const uint32_t b = D::narrow(acc);
-          G = D::widen(b);
-          flag |= D::nonfinite(b);
           if (kReduce) reinterpret_cast<uint16_t*>(a.dst)[k] = (uint16_t)b;
+          rs_epi<DT, false, kEpi>(0.0f, b, inv, sumsq, flag);
         }
-        sq_acc(sumsq, __fmul_rn(G, inv));
       }
     }
+  }
+}
+
+template <int DT, bool kR32, bool kReduce, bool kVec, int NR, int U>
+__global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_constant__ RSArgs a) {
+  if (a.wait_flags) {  // every rank has flattened this bucket (cross-process PEER)
+    if (threadIdx.x == 0) wait_all(a.wait_flags, a.n, a.epoch);
+    __syncthreads();
+  }
+  const float inv = a.st->inv_cur;
+  double sumsq = 0.0;
+  uint32_t flag = 0;
+  if (pow2_at_most_one(inv)) {   // inv = 1/(N S sigma) a power of two (N a power of two)
+    rs_body<DT, kR32, kReduce, kVec, NR, U, 2>(a, inv, sumsq, flag);
+    flag = isfinite(sumsq) ? 0u : 1u;     // G^2 / b^2 of finite values are finite in fp64
+    sumsq *= (double)inv * (double)inv;   // exact
+  } else {
+    rs_body<DT, kR32, kReduce, kVec, NR, U, 1>(a, inv, sumsq, flag);
   }
   grid_publish(sumsq, flag, a.part, a.slot, a.done_sig, a.wait_flags ? a.n : 0, a.epoch);
 }
