@@ -1658,16 +1658,21 @@ int adam_ctas_per_sm(int variant) {
   switch (variant) {
     case 1: return 4;
     case 11: case 21: return 1;
+    case 22: case 23: return 2;
+    case 24: return 3;
     default: return 2;
   }
 }
-bool adam_variant_is_tma(int variant) { return variant == 11 || variant == 21; }
+bool adam_variant_is_tma(int variant) { return variant == 11 || (variant >= 21 && variant <= 24); }
 
 template <int PD, int GD>
 cudaError_t launch_adam_t(const AdamArgs& a, int grid, cudaStream_t s, int variant) {
   switch (variant) {
     case 11: return launch_adam_tma_t<PD, GD, 4096, 2>(a, grid, s);
     case 21: return launch_adam_tma_st_t<PD, GD, 4096, 2>(a, grid, s);
+    case 22: return launch_adam_tma_st_t<PD, GD, 2048, 2>(a, grid, s);   // 2 CTAs/SM
+    case 23: return launch_adam_tma_st_t<PD, GD, 2048, 3>(a, grid, s);   // 2 CTAs/SM
+    case 24: return launch_adam_tma_st_t<PD, GD, 1024, 4>(a, grid, s);   // 3 CTAs/SM
     case 1: k_adam<PD, GD, 4, 1><<<grid, kThreads, 0, s>>>(a); break;
     default: k_adam<PD, GD, 2, 1><<<grid, kThreads, 0, s>>>(a); break;
   }
