@@ -1653,26 +1653,22 @@ cudaError_t launch_adam_tma_st_t(const AdamArgs& a, int grid, cudaStream_t s) {
 // (also measured and dropped -- TMA loads + STG: 2048x4 92.6 %, 2048x2 on 2 CTAs/SM 93.5 %,
 //  1024x{4,6} 61-89 %, 2048x{3,6} 86-91 %, 4096x3 92 %, 6144x2 93 %, 3072x2 92 %, 4096x1 70 %;
 //  TMA loads + TMA stores: 4096x3 94.9 %, 2048x4 95.2 %, 2048x3 98.3 %, 6144x2 95.5 %,
-//  3072x2 94.9 %, 3072x3 95.5 %; register unroll-2 / 3 CTAs 81 %, 1 CTA unroll-4 87 %)
+//  3072x2 94.9 %, 3072x3 95.5 %, and with several CTAs per SM 2048x2 x 2 94.0 %,
+//  2048x3 x 2 92.4 %, 1024x4 x 3 89.9 %; register unroll-2 / 3 CTAs 81 %, 1 CTA unroll-4 87 %)
 int adam_ctas_per_sm(int variant) {
   switch (variant) {
     case 1: return 4;
     case 11: case 21: return 1;
-    case 22: case 23: return 2;
-    case 24: return 3;
     default: return 2;
   }
 }
-bool adam_variant_is_tma(int variant) { return variant == 11 || (variant >= 21 && variant <= 24); }
+bool adam_variant_is_tma(int variant) { return variant == 11 || variant == 21; }
 
 template <int PD, int GD>
 cudaError_t launch_adam_t(const AdamArgs& a, int grid, cudaStream_t s, int variant) {
   switch (variant) {
     case 11: return launch_adam_tma_t<PD, GD, 4096, 2>(a, grid, s);
     case 21: return launch_adam_tma_st_t<PD, GD, 4096, 2>(a, grid, s);
-    case 22: return launch_adam_tma_st_t<PD, GD, 2048, 2>(a, grid, s);   // 2 CTAs/SM
-    case 23: return launch_adam_tma_st_t<PD, GD, 2048, 3>(a, grid, s);   // 2 CTAs/SM
-    case 24: return launch_adam_tma_st_t<PD, GD, 1024, 4>(a, grid, s);   // 3 CTAs/SM
     case 1: k_adam<PD, GD, 4, 1><<<grid, kThreads, 0, s>>>(a); break;
     default: k_adam<PD, GD, 2, 1><<<grid, kThreads, 0, s>>>(a); break;
   }
