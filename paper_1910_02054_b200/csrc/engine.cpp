@@ -673,11 +673,6 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
     c->comm_stream = c->stream;
   }
   if (const char* ev = getenv("ZERO_FLAT_PDL")) c->flat_pdl = atoi(ev) != 0 && c->transport == ZERO_TRANSPORT_LOCAL;
-  // small buckets (a few microseconds of flatten each) gain nothing from overlapping
-  // launches across streams and would pay two extra stream operations per bucket
-  uint64_t max_b = 0;
-  for (const auto& b : c->buckets) max_b = std::max<uint64_t>(max_b, b.size);
-  if (max_b < (1ull << 22)) c->n_flat_streams = 1;
   if (c->flat_pdl) c->n_flat_streams = 1;
   if (const char* ev = getenv("ZERO_FLAT_STREAMS"))
     c->n_flat_streams = std::max(1, std::min(zero_ctx::kMaxFlatStreams, atoi(ev)));
