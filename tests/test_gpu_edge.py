@@ -105,3 +105,25 @@ def test_max_finite_fp16_gradients():
     q.compare()
     p.destroy()
     q.destroy()
+
+
+@pytest.mark.parametrize("n", [1, 3, 4])
+@pytest.mark.parametrize("S", [1000.0, 0.5, 3.0])
+@pytest.mark.parametrize("mode", ["R16", "R32"])
+def test_general_epilogue_path(n, S, mode):
+    """inv = 1/(N*S*sigma) not a power of two (S = 1000, 3; N = 3) or above 1 (S = 0.5):
+    the flatten / reduce-scatter epilogues take the general path (u = fp32(G*inv),
+    per-element flag) instead of the power-of-two one; bit-exact vs the oracle, with
+    clipping active so the norm matters."""
+    if n == 1 and mode == "R32":
+        pytest.skip("R32 is a reduce-scatter storage mode (N > 1)")
+    ts = synth.mlp_layout((120, 70, 30))
+    cfg = OS.AdamConfig.defaults("fp16", dynamic_loss_scale=False, loss_scale=S, max_grad_norm=0.05,
+                                 reduce_mode=mode)
+    p = Pair(Run(ts, n, 2, cfg, cap=1 << 12))
+    for _s in range(3):
+        oinfo, ginfos = p.step()
+        p.compare_info(oinfo, ginfos)
+        assert not oinfo.overflow
+    p.compare()
+    p.destroy()
