@@ -194,6 +194,7 @@ struct zero_ctx {
   uint32_t* cta_flag = nullptr;
   uint32_t* cta_grid = nullptr;
   bool flat_pdl = false;                           // ZERO_FLAT_PDL: one flatten stream, PDL-chained launches
+  bool flat_cta_partials = true;                   // ZERO_FLAT_CTA_PARTIALS=0: last-CTA combine in each flatten
   // ZeRO x MP (R-MP1): per-slot norm weights (0 for MP-replicated buckets on MP rank > 0)
   double* slot_w = nullptr;
   std::vector<double> slot_w_host;
@@ -672,6 +673,7 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   } else {
     c->comm_stream = c->stream;
   }
+  if (const char* ev = getenv("ZERO_FLAT_CTA_PARTIALS")) c->flat_cta_partials = atoi(ev) != 0;
   if (const char* ev = getenv("ZERO_FLAT_PDL")) c->flat_pdl = atoi(ev) != 0 && c->transport == ZERO_TRANSPORT_LOCAL;
   if (c->flat_pdl) c->n_flat_streams = 1;
   if (const char* ev = getenv("ZERO_FLAT_STREAMS"))
@@ -902,7 +904,7 @@ zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads, cud
     a.st = c->st;
     a.part = part;
     a.slot = c->slots + slot;
-    if (epi && c->cta_sum) {
+    if (epi && c->cta_sum && c->flat_cta_partials) {
       a.cta_sum = c->cta_sum + (size_t)slot * kMaxGrid;
       a.cta_flag = c->cta_flag + (size_t)slot * kMaxGrid;
       a.cta_grid = c->cta_grid + slot;
@@ -1222,8 +1224,9 @@ zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev)
   }
   pp = PartialPtrs{};
   if (c->transport == ZERO_TRANSPORT_LOCAL) {
+    const bool cp = c->flat_cta_partials;
     CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream, c->use_slot_w ? c->slot_w : nullptr,
-                           c->cta_sum, c->cta_flag, c->cta_grid));
+                           cp ? c->cta_sum : nullptr, cp ? c->cta_flag : nullptr, cp ? c->cta_grid : nullptr));
     c->launches++;
     pp.p[0] = c->my_partial;
     pp.n = 1;
