@@ -1225,8 +1225,12 @@ zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev)
   pp = PartialPtrs{};
   if (c->transport == ZERO_TRANSPORT_LOCAL) {
     const bool cp = c->flat_cta_partials;
-    CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream, c->use_slot_w ? c->slot_w : nullptr,
-                           cp ? c->cta_sum : nullptr, cp ? c->cta_flag : nullptr, cp ? c->cta_grid : nullptr));
+    if (cp && c->n_slots <= kMaxGrid)   // the flattens left per-CTA partials; part_compute is free
+      CK(launch_decide_local_slots(c->n_slots, c->my_partial, c->comm_stream, c->use_slot_w ? c->slot_w : nullptr,
+                                   c->cta_sum, c->cta_flag, c->cta_grid, c->part_compute));
+    else
+      CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream, c->use_slot_w ? c->slot_w : nullptr,
+                             cp ? c->cta_sum : nullptr, cp ? c->cta_flag : nullptr, cp ? c->cta_grid : nullptr));
     c->launches++;
     pp.p[0] = c->my_partial;
     pp.n = 1;

@@ -1093,6 +1093,53 @@ __global__ void __launch_bounds__(1024) k_decide_local(Slot* slots, int n, RankP
   }
 }
 
+// N_d = 1 with per-CTA flatten partials: one CTA per bucket slot reduces that slot's
+// partials (block tree), then the last CTA to finish combines the slots in slot order
+__global__ void __launch_bounds__(kThreads) k_decide_local_slots(const double* slot_w, const double* cta_sum,
+                                                                 const uint32_t* cta_flag, const uint32_t* cta_grid,
+                                                                 GridPartials* part, RankPartial* out) {
+  __shared__ bool is_last;
+  const int i = blockIdx.x;
+  const uint32_t g = cta_grid[i];
+  const double* cs = cta_sum + (size_t)i * kMaxGrid;
+  const uint32_t* cf = cta_flag + (size_t)i * kMaxGrid;
+  double s = 0.0;
+  uint32_t f = 0;
+  for (uint32_t c = threadIdx.x; c < g; c += blockDim.x) {
+    s += cs[c];
+    f |= cf[c];
+  }
+  block_reduce(s, f);
+  if (threadIdx.x == 0) {
+    part->sumsq[i] = slot_w ? slot_w[i] * s : s;   // weights 0/1 (ZeRO x MP): exact
+    part->flag[i] = f;
+    __threadfence();
+    is_last = atomicAdd(&part->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double a = 0.0;
+  uint32_t b = 0;
+  for (unsigned j = threadIdx.x; j < gridDim.x; j += blockDim.x) {
+    a += __ldcg(&part->sumsq[j]);
+    b |= __ldcg(&part->flag[j]);
+  }
+  block_reduce(a, b);
+  if (threadIdx.x == 0) {
+    out->sumsq = a;
+    out->flag = b ? 1.0 : 0.0;
+    part->ticket = 0;
+  }
+}
+
+cudaError_t launch_decide_local_slots(int n_slots, RankPartial* out, cudaStream_t s, const double* slot_w,
+                                      const double* cta_sum, const uint32_t* cta_flag, const uint32_t* cta_grid,
+                                      GridPartials* part) {
+  k_decide_local_slots<<<n_slots, kThreads, 0, s>>>(slot_w, cta_sum, cta_flag, cta_grid, part, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_decide_local(Slot* slots, int n_slots, RankPartial* out, cudaStream_t s, const double* slot_w,
                                 const double* cta_sum, const uint32_t* cta_flag, const uint32_t* cta_grid) {
   // 32 warps: one per bucket slot at a time for the N_d = 1 per-CTA partials

@@ -193,6 +193,10 @@ cudaError_t launch_wait(const WaitArgs& a, cudaStream_t s);
 cudaError_t launch_handshake(const SigArgs& a, const uint64_t* my_flags, uint64_t timeout_ns, uint32_t* result,
                              cudaStream_t s);
 cudaError_t launch_push_partial(const PushArgs& a, cudaStream_t s);
+// N_d = 1 per-CTA flatten partials, one CTA per slot + a last-CTA combine (n_slots <= kMaxGrid)
+cudaError_t launch_decide_local_slots(int n_slots, RankPartial* out, cudaStream_t s, const double* slot_w,
+                                      const double* cta_sum, const uint32_t* cta_flag, const uint32_t* cta_grid,
+                                      GridPartials* part);
 // zero_step_begin: sum the partials of pp (waiting on its flags) into *out
 cudaError_t launch_combine_partials(const PartialPtrs& pp, RankPartial* out, cudaStream_t s);
 cudaError_t launch_decide_global(const PartialPtrs& partials, DevState* st, DecideParams p, cudaStream_t s);
