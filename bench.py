@@ -1,30 +1,44 @@
 #!/usr/bin/env python
 """bench.py -- ZeRO-DP step throughput on B200 (BASELINE.json metric).
 
-One "step" = one pass of the whole hot path (SURVEY §8a rows a1-a6) over one
+One "step" = one pass of the whole hot path (SURVEY §8a rows a1-a6/a7) over one
 batch of synthetic gradients: for every bucket (in reverse, as backward produces
 them) zero_reduce_grads (flatten/cast/scale + reduce-scatter + overflow/norm
 epilogue), then zero_step (global decision, fused partitioned Adam + recast into
-the all-gather buffer, all-gather).  Inputs are resident in HBM when the timed
-region starts; the working set (~25 GB at 1.5B) is >> the 126 MB L2, so no L2
-flush is needed between steps (stated in config.l2).
+the all-gather buffer, all-gather); at stage 3 the per-layer gathers of the
+forward and backward as well.  Inputs are resident in HBM when the timed
+region starts; the working set (>= 25 GB) is >> the 126 MB L2, so no L2 flush is
+needed between steps (stated in config.l2).
 
-Default (N=1): GPT-2 1.5B layout (Psi = 1,557,611,200), ZeRO stage 1,
-bf16 params/grads, fp32 Adam states.  Under torchrun (N>1) every rank runs the
-same layout over NCCL (strong scaling: the model is fixed).
+Default (N=1): the 7.5B layout of the paper's Fig. 1 (Psi = 7,500,000,000,
+120 GB of model states), ZeRO stage 2 (P_os+g), bf16 params/grads with fp32 Adam
+states -- the largest BASELINE config that fits one GPU.  The same layout in fp16
+with dynamic loss scaling (the paper's precision; reading c-4) is timed
+as a second key ("fp16_dynamic").
 
-  python bench.py [--steps K] [--warmup W] [--config gpt2_1.5b|gpt_7.5b|mlp1m] [--stage S]
+Multi-GPU (strong scaling: the model is fixed): `--gpus N` under torchrun reads
+WORLD_SIZE/RANK/LOCAL_RANK (WORLD_SIZE must equal N); without torchrun, `--gpus N`
+spawns the N ranks itself through torch.distributed.run.  ZERO_BENCH_SAME_DEVICE=1
+puts every rank on cuda:0 (a functional check of the N>1 flow on a 1-GPU box; the
+ranks time-slice one GPU, so its numbers are not throughput).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config gpt_7.5b|gpt2_1.5b|gpt_60b|mlp1m] [--stage S]
   python bench.py --impl reference      # the CPU oracle on a bounded sample (the reference arm)
 """
 from __future__ import annotations
 
 import argparse
+import gc
+import glob
 import json
 import math
 import os
+import re
+import socket
 import statistics
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 
@@ -32,31 +46,63 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "ZeRO step Gparams/s at 1/2/4/8 B200; % of HBM+NVLink roofline"
-NVLINK_GBS = 770.0   # per direction per GPU: the measured peer copy (B200_PROFILING.md); 900 nominal
+NVLINK_GBS = 770.0        # per direction per GPU: the measured peer copy (B200_PROFILING.md)
+NVLINK_NOMINAL_GBS = 900.0
+DEFAULT_STAGE = {"gpt2_1.5b": 1, "gpt_7.5b": 2, "gpt_60b": 3, "mlp1m": 2}
+# transports with a passing multi-device parity test in this repo's history:
+# the CUDA-IPC PEER path is bit-exact across processes (tests/test_gpu_ipc.py); NCCL at
+# N > 1 has only the gated tests/test_gpu_multidevice.py, never run on a multi-GPU box
+VERIFIED_TRANSPORTS = {"peer"}
 
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="ranks (default: WORLD_SIZE, else 1); without torchrun, N > 1 spawns the ranks")
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="gpt2_1.5b")
+    ap.add_argument("--config", default="gpt_7.5b")
     ap.add_argument("--stage", type=int, default=None)
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"])
+    ap.add_argument("--reduce-mode", default="R16", choices=["R16", "R32"])
     ap.add_argument("--cap", type=int, default=1 << 26)
     ap.add_argument("--align", type=int, default=64)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="N>1: peer = CUDA-IPC pull reduce-scatter + Adam-fused all-gather (default); nccl = library collectives")
+    ap.add_argument("--allow-unverified", action="store_true",
+                    help="run a transport without a passing multi-device parity test (the line says so)")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--graph", action="store_true",
                     help="capture one whole step (all zero_reduce_grads + zero_step) in a CUDA graph and time replays")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-fp16-key", action="store_true", help="skip the fp16 dynamic-loss-scale second run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cpu-parallel", action="store_true", help="skip the all-cores oracle baseline")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     return ap.parse_args()
+
+
+def world_size(args) -> int:
+    """The number of ranks of this run.  Under torchrun WORLD_SIZE rules and must equal
+    --gpus when both are given; without torchrun, --gpus N > 1 re-launches this script
+    as N ranks (torch.distributed.run on 127.0.0.1) and exits with their status."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if args.gpus is not None and int(ws) != args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}\n")
+            raise SystemExit(2)
+        return int(ws)
+    n = args.gpus or 1
+    if n == 1 or args.impl == "reference":
+        return n
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd))
 
 
 def peaks():
@@ -230,17 +276,23 @@ def oracle_parallel_run(tensors, dtype: str, seed: int, budget_s: float, procs: 
     return work / dt / 1e9, desc
 
 
-def run_reference(args, tensors, psi_total):
+def run_reference(args, tensors, psi_total, world):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     steps, warmup = args.steps, args.warmup
     budget = min(150.0, 1.2 * (steps + warmup))
     value, desc, n, dt = oracle_sample_run(tensors, args.dtype, args.seed, steps, warmup, budget)
+    ms_sample = dt / steps * 1e3
     line = {
-        "metric": METRIC, "value": value, "unit": "Gparams/s", "n_gpus": args.gpus, "steps": steps,
-        "warmup": warmup, "ms_per_step": dt / steps * 1e3 * psi_total / n, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "metric": METRIC, "value": value, "unit": "Gparams/s", "n_gpus": world, "steps": steps,
+        "warmup": warmup,
+        # measured: one timed step = the oracle over the bounded sample (sample_params elements)
+        "ms_per_step": ms_sample,
+        "ms_per_step_kind": "measured per sample step (each step is the oracle over sample_params elements)",
+        "ms_per_full_step_extrapolated": ms_sample * psi_total / n,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
         "config": {"workload": f"{args.config} layout, ZeRO stage {args.stage}", "psi": psi_total,
                    "param_dtype": args.dtype, "sample_params": n},
         "impl": "reference",
@@ -253,204 +305,269 @@ def run_reference(args, tensors, psi_total):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def nccl_info_summary(log_glob: str, world: int):
+    """What NCCL's INFO log says about the communicators of this process (comm size, NVLS)."""
+    nr, nvls = [], False
+    for p in glob.glob(log_glob):
+        try:
+            with open(p, errors="replace") as f:
+                for line in f:
+                    m = re.search(r"\bn[Rr]anks[ =](\d+)", line)
+                    if m:
+                        nr.append(int(m.group(1)))
+                    if "NVLS" in line and "NVLS multicast support is not available" not in line:
+                        nvls = True
+        except OSError:
+            pass
+    return {"nranks_seen": sorted(set(nr)), "comm_nranks_ok": bool(nr) and world in nr, "nvls_mentioned": nvls}
+
+
 def main():
     args = parse()
+    world = world_size(args)
     import synth
     tensors = synth.CONFIGS[args.config]()
     if args.stage is None:
-        args.stage = {"gpt2_1.5b": 1, "gpt_7.5b": 2, "gpt_60b": 3, "mlp1m": 2}.get(args.config, 1)
+        args.stage = DEFAULT_STAGE.get(args.config, 1)
     psi_total = synth.psi(tensors)
     if args.impl == "reference":
-        return run_reference(args, tensors, psi_total)
+        return run_reference(args, tensors, psi_total, world)
+
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    same_dev = os.environ.get("ZERO_BENCH_SAME_DEVICE") == "1"
+    transport = "local" if world == 1 else args.transport
+    verified = transport == "local" or transport in VERIFIED_TRANSPORTS
+    if not verified and not args.allow_unverified:
+        sys.stderr.write(f"bench.py: the {transport} transport has no passing multi-device parity test; "
+                         "pass --allow-unverified to time it anyway\n")
+        raise SystemExit(3)
+    if same_dev and transport == "nccl":
+        raise SystemExit("NCCL cannot place two ranks on one GPU; use --transport peer")
+    nccl_log = None
+    if world > 1 and not same_dev:     # NCCL INFO lines go to a file (never to stdout)
+        nccl_log = os.path.join(tempfile.gettempdir(), f"zero_bench_nccl_{os.environ.get('MASTER_PORT', '0')}")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", nccl_log + ".%h.%p.log")
 
     import torch
     import torch.distributed as dist
-    from paper_1910_02054_b200 import ZeroConfig, ZeroEngine, nccl_comm_ptr
+    from paper_1910_02054_b200 import ZeroConfig, ZeroEngine, comm_elems_per_rank, nccl_comm_ptr
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    # ZERO_BENCH_SAME_DEVICE=1: every rank on cuda:0 (functional check of the N>1 flow on a
-    # 1-GPU box; the ranks time-slice the GPU, so its numbers are not throughput)
-    same_dev = os.environ.get("ZERO_BENCH_SAME_DEVICE") == "1"
     if same_dev:
         local = 0
-        if args.transport == "nccl":
-            raise SystemExit("NCCL cannot place two ranks on one GPU; use --transport peer")
+    elif torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} ranks but {torch.cuda.device_count()} visible GPUs "
+                         "(ZERO_BENCH_SAME_DEVICE=1 for a functional run on one GPU)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    gloo = None
     if world > 1:
         if same_dev:
             dist.init_process_group("gloo")
+            gloo = dist.group.WORLD
         else:
             dist.init_process_group("nccl", device_id=dev)
             warm = torch.ones(1, device=dev)
             dist.all_reduce(warm)
+            gloo = dist.new_group(backend="gloo")
         torch.cuda.synchronize()
     # the graph mode captures on a side stream (capture is not allowed on the legacy stream)
     stream = torch.cuda.Stream(dev) if args.graph else torch.cuda.current_stream(dev)
     torch.cuda.set_stream(stream)
-    tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float16
-
-    # phase events cannot be timed inside a captured graph: --graph runs without them
-    cfg = ZeroConfig.defaults(args.dtype, timing=not args.graph)
-    if args.dtype == "fp16":
-        cfg.loss_scale = 1.0        # inputs are generated unscaled; keep S fixed so no step overflows
-        cfg.dynamic_loss_scale = False
-    transport = "local" if world == 1 else args.transport
-    fallback_note = None
-
-    def make_engine(tr):
-        comm = nccl_comm_ptr(dist.group.WORLD) if tr == "nccl" else 0
-        e = ZeroEngine([t.numel for t in tensors], [t.layer for t in tensors], world, rank, args.stage, cfg,
-                       tr, comm, stream, args.align, args.cap, dev)
-        if tr == "peer":
-            e.link_peers(dist.new_group(backend="gloo"))   # exchange CUDA IPC handles, open the peer table
-        return e
-
-    try:
-        eng = make_engine(transport)
-        ok = 1
-    except Exception as exc:  # e.g. CUDA IPC not permitted in this container
-        eng, ok, fallback_note = None, 0, f"{transport} transport failed ({exc}); fell back to nccl"
-    if world > 1:                                           # every rank must agree on the transport
-        flag = torch.tensor([ok], dtype=torch.int32, device=dev if not same_dev else "cpu")
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        if int(flag.item()) == 0 and transport != "nccl" and not same_dev:
-            if eng is not None:
-                eng.destroy()
-            fallback_note = fallback_note or "a peer rank failed to link; fell back to nccl"
-            transport = "nccl"
-            eng = make_engine("nccl")
-    if eng is None:
-        raise SystemExit(fallback_note)
-    info = eng.info
-    nb = info.n_buckets
-
-    # fp32 masters, loaded in chunks of <= 2^29 elements (bounded temporary memory)
-    chunk, cur = [], 0
-    for i, t in enumerate(tensors):
-        chunk.append(i)
-        cur += t.numel
-        if cur >= (1 << 29) or i == len(tensors) - 1:
-            masters = synth.gpu_masters(tensors, args.seed, dev, only=set(chunk))
-            eng.load_master(masters)
-            torch.cuda.synchronize()
-            del masters
-            chunk, cur = [], 0
-    grad_buf, grads = synth.gpu_grads_flat(tensors, args.seed, rank, 0, tdt, dev)
-    eng.set_grads(grads)
-    torch.cuda.synchronize()
-
-    layer_ids = sorted({b.layer for b in eng.buckets})
-    layer_buckets = {L: [k for k, b in enumerate(eng.buckets) if b.layer == L] for L in layer_ids}
-
-    def one_step():
-        if args.stage == 3:
-            # SURVEY §8d step-only protocol for P_os+g+p: gather every layer for the
-            # forward (prefetching the next), then in reverse for the backward, each layer
-            # followed by its buckets' reduce-scatter; release after use
-            for L in layer_ids:
-                eng.gather_params(L)
-                eng.release_params(L)
-            for L in reversed(layer_ids):
-                eng.gather_params(L)
-                for k in reversed(layer_buckets[L]):
-                    eng.reduce_grads(k)
-                eng.release_params(L)
-        else:
-            for k in reversed(range(nb)):
-                eng.reduce_grads(k)
-        eng.step()
 
     def barrier():
         if world > 1:
             dist.barrier() if same_dev else dist.barrier(device_ids=[local])
 
-    for _ in range(max(args.warmup, 3)):
-        one_step()
-    torch.cuda.synchronize()
-    barrier()
-    eng.timing()                           # reset the phase accumulators
-    launches0 = eng.timing().kernel_launches
-    graph, launches_per_step = None, None
-    if args.graph:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
+    def build(dtype):
+        """One rank's context for `dtype`: fp32 masters loaded, gradients generated at the
+        loss scale S (fp16: dynamic, S0 = 2^16; bf16: static S = 1; reading c-4)."""
+        cfg = ZeroConfig.defaults(dtype, timing=not args.graph, reduce_mode=args.reduce_mode)
+        comm = nccl_comm_ptr(dist.group.WORLD) if transport == "nccl" else 0
+        eng = ZeroEngine([t.numel for t in tensors], [t.layer for t in tensors], world, rank, args.stage, cfg,
+                         transport, comm, stream, args.align, args.cap, dev)
+        if transport == "peer":
+            eng.link_peers(gloo)      # exchange CUDA IPC handles, open the peer table (fails loudly)
+        chunk, cur = [], 0           # fp32 masters in chunks of <= 2^29 elements
+        for i, t in enumerate(tensors):
+            chunk.append(i)
+            cur += t.numel
+            if cur >= (1 << 29) or i == len(tensors) - 1:
+                masters = synth.gpu_masters(tensors, args.seed, dev, only=set(chunk))
+                eng.load_master(masters)
+                torch.cuda.synchronize()
+                del masters
+                chunk, cur = [], 0
+        tdt = torch.bfloat16 if dtype == "bf16" else torch.float16
+        grad_buf, grads = synth.gpu_grads_flat(tensors, args.seed, rank, 0, tdt, dev, scale=cfg.loss_scale)
+        eng.set_grads(grads)
+        torch.cuda.synchronize()
+        return eng, cfg, grad_buf, grads
+
+    def make_step(eng):
+        nb = eng.info.n_buckets
+        layer_ids = sorted({b.layer for b in eng.buckets})
+        layer_buckets = {L: [k for k, b in enumerate(eng.buckets) if b.layer == L] for L in layer_ids}
+
+        def one_step():
+            if args.stage == 3:
+                # SURVEY §8d step-only protocol for P_os+g+p (P:476): gather every layer for the
+                # forward (prefetching the next), then in reverse for the backward, each layer
+                # followed by its buckets' reduce-scatter; release after use
+                for L in layer_ids:
+                    eng.gather_params(L)
+                    eng.release_params(L)
+                for L in reversed(layer_ids):
+                    eng.gather_params(L)
+                    for k in reversed(layer_buckets[L]):
+                        eng.reduce_grads(k)
+                    eng.release_params(L)
+            else:
+                for k in reversed(range(nb)):
+                    eng.reduce_grads(k)
+            eng.step()
+        return one_step
+
+    def timed(eng, steps, sample_clocks=True):
+        one_step = make_step(eng)
+        for _ in range(max(args.warmup, 3)):
             one_step()
-        launches_per_step = eng.timing().kernel_launches - launches0
-        for _ in range(2):
-            graph.replay()
         torch.cuda.synchronize()
         barrier()
-    run_step = graph.replay if graph is not None else one_step
+        eng.timing()                           # reset the phase accumulators
+        launches0 = eng.timing().kernel_launches
+        comm0 = eng.comm_counters()
+        graph, launches_per_step = None, None
+        if args.graph:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                one_step()
+            launches_per_step = eng.timing().kernel_launches - launches0
+            for _ in range(2):
+                graph.replay()
+            torch.cuda.synchronize()
+            barrier()
+        run_step = graph.replay if graph is not None else one_step
+        clocks = ClockSampler(local) if sample_clocks else None
+        if clocks:
+            clocks.start()
+            time.sleep(0.3)
+        barrier()
+        torch.cuda.synchronize()
+        comm1 = eng.comm_counters()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        if clocks:
+            clocks.mark(True)
+        evs[0].record(stream)
+        for i in range(steps):
+            run_step()
+            evs[i + 1].record(stream)      # per-step boundaries (median / p10 / p90)
+        torch.cuda.synchronize()
+        if clocks:
+            clocks.mark(False)
+        barrier()
+        comm2 = eng.comm_counters()
+        ms = max_over_ranks(evs[0].elapsed_time(evs[-1]) / steps, dev)
+        per_step = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(steps))
+        clk = clocks.stop() if clocks else None
+        tm = eng.timing()
+        launches = tm.kernel_launches - launches0 if graph is None else launches_per_step * steps
+        rec = eng.step_info()
+        if graph is None:
+            sent = [(getattr(comm2, f) - getattr(comm1, f)) / steps for f in ("reduce_scatter", "all_gather", "all_reduce")]
+        else:   # replays do not pass through the host counters: the captured step's counts
+            sent = [getattr(comm1, f) - getattr(comm0, f) for f in ("reduce_scatter", "all_gather", "all_reduce")]
+        return {"ms": ms, "per_step": per_step, "tm": tm, "launches": launches, "clocks": clk, "rec": rec,
+                "graph": graph is not None, "sent": sent}
 
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    barrier()
-    torch.cuda.synchronize()
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    clocks.mark(True)
-    evs[0].record(stream)
-    for i in range(args.steps):
-        run_step()
-        evs[i + 1].record(stream)      # per-step boundaries (median / p10 / p90)
-    torch.cuda.synchronize()
-    clocks.mark(False)
-    barrier()
-    ms = max_over_ranks(evs[0].elapsed_time(evs[-1]) / args.steps, dev)
-    per_step = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps))
+    eng, cfg, grad_buf, grads = build(args.dtype)
+    info = eng.info
+    nb = info.n_buckets
+    res = timed(eng, args.steps)
+    rec = res["rec"]
+    assert rec.overflow == 0 and rec.t >= args.steps, "benchmark steps must not be skipped"
+    ms, tm = res["ms"], res["tm"]
+    per_step = res["per_step"]
 
     def pct(q):
         return per_step[min(len(per_step) - 1, int(q * (len(per_step) - 1) + 0.5))]
-    clk = clocks.stop()
-    tm = eng.timing()
-    gpu_launches = tm.kernel_launches - launches0 if graph is None else launches_per_step * args.steps
-    info_rec = eng.step_info()
-    assert info_rec.overflow == 0 and info_rec.t >= args.steps, "benchmark steps must not be skipped"
 
     value = psi_total / (ms * 1e-3) / 1e9
-
-    # roofline of the dominant kernel (fused Adam), measured live with events on its stream
     hbm_peak, peak_kind = peaks()
-    S_e = info.psi_padded if args.stage == 0 else info.shard
-    g_bytes = 4 if (cfg.reduce_mode == "R32" and world > 1) else 2
-    adam_bytes = (24 + g_bytes + 2) * S_e     # p32, m, v read+write, G read, p16 write
-    adam_ms = tm.adam_ms / tm.steps if tm.steps else None
-    adam_gbs = adam_bytes / (adam_ms * 1e-3) / 1e9 if adam_ms else None
+    N = world
+    pp = info.psi_padded
+    S_e = pp if args.stage == 0 else info.shard
+    r32 = cfg.reduce_mode == "R32" and N > 1
+    g_bytes = 4 if r32 else 2
+
+    def adam_roofline(tm_):
+        """achieved HBM GB/s of the fused Adam, CUDA events on its stream over the timed region"""
+        adam_bytes = (24 + g_bytes + 2) * S_e      # p32, m, v read+write, G read, p16 write
+        adam_ms = tm_.adam_ms / tm_.steps if tm_.steps else None
+        gbs = adam_bytes / (adam_ms * 1e-3) / 1e9 if adam_ms else None
+        return adam_bytes, adam_ms, gbs
+
+    adam_bytes, adam_ms, adam_gbs = adam_roofline(tm)
     traffic, t_elems = ncu_traffic("k_adam")
     if traffic is not None and t_elems:
         traffic = traffic * S_e / t_elems   # the capture's bytes per element x this launch's elements
     reduce_ms = tm.reduce_ms / tm.steps if tm.steps else None
-    pp = info.psi_padded
-    # step roofline: sum over phases of max(HBM bytes / BW_HBM, NVLink bytes / BW_NVL)
-    N = world
 
-    def t_roof_at(hbm_gbs):
+    def t_roof_at(hbm_gbs, nvl_gbs=NVLINK_GBS):
+        # step roofline (SURVEY §8d): sum over phases of max(HBM bytes / BW_HBM, NVLink bytes / BW_NVL)
         hbm = hbm_gbs * 1e9
         t_flat = 4 * pp / hbm
+        adam = (24 + g_bytes + 2) * pp / N
         if N == 1:
-            return t_flat + 28 * pp / hbm
-        nvl = 2 * pp * (N - 1) / N / (NVLINK_GBS * 1e9)      # one RS or one AG of Psi' 16-bit elements
+            return t_flat + adam / hbm
+        nvl = 2 * pp * (N - 1) / N / (nvl_gbs * 1e9)      # one RS or one AG of Psi' 16-bit elements
+        nvl_rs = nvl * (2 if (r32 and transport == "nccl") else 1)
         if args.stage == 3:                                   # [AG fwd] -> [flatten + RS + AG bwd] -> [Adam]
-            return max(2 * pp / hbm, nvl) + max((4 * pp + 2 * pp + 2 * pp / N) / hbm, 2 * nvl) + 28 * pp / N / hbm
-        t_rs = max((2 * pp + 2 * pp / N) / hbm, nvl)
+            return max(2 * pp / hbm, nvl) + max((4 * pp + 2 * pp + 2 * pp / N) / hbm, nvl_rs + nvl) + adam / hbm
+        t_rs = max((2 * pp + 2 * pp / N) / hbm, nvl_rs)
         if args.stage == 0:                                   # [flatten] -> [RS] -> [AG of the sums] -> [full Adam]
             return t_flat + t_rs + max(2 * pp / hbm, nvl) + 28 * pp / hbm
-        return t_flat + t_rs + max((28 * pp / N + 2 * pp) / hbm, nvl)   # [flatten] -> [RS] -> [Adam || AG]
+        return t_flat + t_rs + max((adam + 2 * pp) / hbm, nvl)   # [flatten] -> [RS] -> [Adam || AG]
     t_roof = t_roof_at(hbm_peak)
+
+    # counted elements sent per rank per step vs the paper's closed forms (P:445, P:473, P:478)
+    counted = sum(res["sent"])
+    closed = comm_elems_per_rank(pp, N, args.stage)
+    comm = {"elems_sent_per_step": {"reduce_scatter": res["sent"][0], "all_gather": res["sent"][1],
+                                    "all_reduce": res["sent"][2], "total": counted},
+            "closed_form": closed, "closed_form_name": "3 Psi'(N-1)/N" if args.stage == 3 else "2 Psi'(N-1)/N",
+            "equal": counted == closed}
+    if N > 1:
+        # bus bandwidth in the nccl-tests convention, (S / t) (N-1)/N with S = the 16-bit buffer
+        # (2 Psi' bytes); the phases overlap HBM work (the flattens; the Adam of the fused AG)
+        S_bytes = 2 * pp
+        ag_ms = (tm.ag_ms / tm.steps if tm.steps else None) if transport == "nccl" else adam_ms
+        comm["rs_phase_ms"] = reduce_ms
+        comm["rs_busbw_gbs"] = S_bytes / (reduce_ms * 1e-3) / 1e9 * (N - 1) / N if reduce_ms else None
+        comm["ag_phase_ms"] = ag_ms
+        comm["ag_busbw_gbs"] = S_bytes / (ag_ms * 1e-3) / 1e9 * (N - 1) / N if ag_ms else None
+        comm["ag_phase_kind"] = "nccl all-gather group" if transport == "nccl" else "fused into the Adam kernel's bulk stores"
+        comm["busbw_ref_gbs"] = {"nominal": NVLINK_NOMINAL_GBS, "measured_peer_copy": NVLINK_GBS}
+        for k in ("rs", "ag"):
+            v = comm.get(f"{k}_busbw_gbs")
+            comm[f"{k}_frac_of_nominal"] = v / NVLINK_NOMINAL_GBS if v else None
+
     line = {
         "metric": METRIC, "value": value, "unit": "Gparams/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms,
-        "ms_per_step_p10_p50_p90": [pct(0.1), pct(0.5), pct(0.9)] if world == 1 else None,
+        "ms_per_step_p10_p50_p90": [pct(0.1), pct(0.5), pct(0.9)],
         "higher_is_better": True, "scaling": "strong",
+        # dtype = the arithmetic type the path computes in (fp32 Adam / fp32 sums); the
+        # parameter and gradient storage type is config.param_dtype
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.config} layout, ZeRO stage {args.stage}", "psi": psi_total,
                    "psi_padded": pp, "buckets": nb, "bucket_cap_elems": args.cap, "align_elems": args.align,
-                   "param_dtype": args.dtype, "adam_state_dtype": "fp32", "reduce_mode": cfg.reduce_mode,
-                   "transport": transport, "parallelism": f"zero{args.stage}-dp{world}",
-                   "transport_note": fallback_note,
+                   "param_dtype": args.dtype, "loss_scale": "dynamic, S0 = 2^16" if args.dtype == "fp16" else "static 1",
+                   "adam_state_dtype": "fp32", "reduce_mode": cfg.reduce_mode,
+                   "transport": transport, "transport_verified": verified, "parallelism": f"zero{args.stage}-dp{world}",
+                   "same_device_ranks": bool(same_dev and world > 1),
                    "l2": "no flush: >= 25 GB streamed per step vs 126 MB L2"},
         "roofline": {"bound": "hbm", "kernel": "k_adam (fused partitioned Adam + recast)",
                      "achieved": adam_gbs, "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
@@ -460,82 +577,51 @@ def main():
                      "note": None if adam_ms else "--graph: per-kernel events are not recorded inside the graph"},
         "step_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
                           "hbm_gbs": hbm_peak, "nvlink_gbs": NVLINK_GBS if N > 1 else None,
-                          "frac_at_spec_hbm_8tbs": t_roof_at(8000.0) * 1e3 / ms,
-                          "hbm_gbs": hbm_peak, "nvlink_gbs": NVLINK_GBS if N > 1 else None,
+                          "frac_at_spec_hbm_8tbs": t_roof_at(8000.0, NVLINK_NOMINAL_GBS) * 1e3 / ms,
                           "reduce_phase_ms": reduce_ms, "flatten_gbs": 4 * pp / (reduce_ms * 1e-3) / 1e9
                           if (N == 1 and reduce_ms) else None},
-        "cuda_graph": bool(graph is not None),
-        "clocks": clk,
-        "gpu_launches": int(gpu_launches),
+        "comm": comm,
+        "cuda_graph": res["graph"],
+        "clocks": res["clocks"],
+        "gpu_launches": int(res["launches"]),
     }
+    if nccl_log:
+        line["nccl_info"] = nccl_info_summary(nccl_log + ".*.log", world)
 
     # e2e through the public API with HOST buffers: H2D of the step's gradients from
     # pinned memory + the step + D2H of the step record, every step
     if not args.no_e2e:
-        # Every step copies that step's gradients H2D from pinned host memory and reads
-        # the step record D2H.  The copy of step s+1 (copy stream, second device buffer)
-        # overlaps step s; the host reads step s's record before issuing step s+2.
-        host = torch.empty(grad_buf.numel(), dtype=grad_buf.dtype, pin_memory=True)
-        host.copy_(grad_buf)
-        bufs = [grad_buf, torch.empty_like(grad_buf)]
-        views = [grads, [bufs[1][o:o + t.numel] for t, o in zip(tensors, synth.tensor_offsets(tensors))]]
-        copy_stream = torch.cuda.Stream(dev)
-        copied = [torch.cuda.Event(), torch.cuda.Event()]
-        consumed = [torch.cuda.Event(), torch.cuda.Event()]
-        rec = eng._info_host
-        torch.cuda.synchronize()
-        # the PCIe bound of this leg: one pinned H2D of the step's gradients, alone
-        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(copy_stream):
-            h0.record(copy_stream)
-            bufs[1].copy_(host, non_blocking=True)
-            h1.record(copy_stream)
-        torch.cuda.synchronize()
-        h2d_ms = h0.elapsed_time(h1)
-        barrier()
-        K = args.e2e_steps
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0 = time.perf_counter()
-        e0.record(copy_stream)
-        with torch.cuda.stream(copy_stream):
-            bufs[0].copy_(host, non_blocking=True)
-            copied[0].record(copy_stream)
-        for s in range(K):
-            cur = s % 2
-            stream.wait_event(copied[cur])
-            eng.set_grads(views[cur])
-            for k in reversed(range(nb)):
-                eng.reduce_grads(k)
-            eng.step()                              # + 32-byte step record D2H into pinned memory
-            consumed[cur].record(stream)            # joined: the flattens have read bufs[cur]
-            if s + 1 < K:
-                nxt = (s + 1) % 2
-                copy_stream.wait_event(consumed[nxt])
-                with torch.cuda.stream(copy_stream):
-                    bufs[nxt].copy_(host, non_blocking=True)
-                    copied[nxt].record(copy_stream)
-            stream.synchronize()                    # the host reads step s's result
-            _ = bytes(rec.numpy()[:32])
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / K, dev)
-        e2e_dev_ms = max_over_ranks(e0.elapsed_time(e1) / K, dev)
-        eng.set_grads(grads)
-        line["e2e"] = {"value": psi_total / (e2e_ms * 1e-3) / 1e9, "unit": "Gparams/s",
-                       "h2d_bytes_per_step": int(grad_buf.numel() * grad_buf.element_size()),
-                       "d2h_bytes_per_step": 32, "ms_per_step": e2e_ms, "steps": K,
-                       "device_ms_per_step": e2e_dev_ms,
-                       "h2d_alone_ms": h2d_ms,
-                       "h2d_gbs": grad_buf.numel() * grad_buf.element_size() / (h2d_ms * 1e-3) / 1e9,
-                       "frac_of_h2d_bound": max(h2d_ms, ms) / e2e_ms,
-                       "note": "value from the host wall clock (device_ms_per_step: CUDA events from the first H2D "
-                               "to the last step's end); H2D of step s+1 overlaps step s (double-buffered)"}
+        try:
+            line["e2e"] = run_e2e(args, eng, grad_buf, grads, tensors, stream, dev, psi_total, ms, barrier)
+        except RuntimeError as exc:     # e.g. pinned host memory exhausted by N ranks
+            line["e2e"] = {"value": None, "unit": "Gparams/s", "note": f"not measured: {exc}"}
+            barrier()
+
+    # the same layout in fp16 with dynamic loss scaling (the paper's precision)
+    if args.dtype == "bf16" and not args.no_fp16_key and not args.graph:
+        eng.destroy()
+        del eng, grad_buf, grads
+        gc.collect()
+        torch.cuda.empty_cache()
+        e16, c16, gb16, g16 = build("fp16")
+        r16 = timed(e16, args.steps, sample_clocks=False)
+        _, a16_ms, a16_gbs = adam_roofline(r16["tm"])
+        line["fp16_dynamic"] = {
+            "value": psi_total / (r16["ms"] * 1e-3) / 1e9, "unit": "Gparams/s", "ms_per_step": r16["ms"],
+            "loss_scale": "dynamic (S0 = 2^16, x2 per 1000 good steps, x1/2 on overflow)",
+            "loss_scale_last": r16["rec"].loss_scale, "overflow_last": r16["rec"].overflow, "t_last": r16["rec"].t,
+            "step_roofline_frac": t_roof * 1e3 / r16["ms"],
+            "adam_gbs": a16_gbs, "adam_frac": a16_gbs / hbm_peak if a16_gbs else None,
+            "gpu_launches": int(r16["launches"])}
+        assert r16["rec"].overflow == 0 and r16["rec"].loss_scale == 2.0 ** 16, "fp16 run overflowed"
+        e16.destroy()
+        del e16, gb16, g16
 
     if rank == 0 and not args.no_cpu_baseline:
         v, desc, n, dt = oracle_sample_run(tensors, args.dtype, args.seed, 2, 0, args.cpu_budget_s)
         line["cpu_baseline"] = {"value": v, "unit": "Gparams/s", "cores": 1, "kind": "oracle", "sample": desc}
         procs = len(os.sched_getaffinity(0))
-        if procs > 1 and not args.no_cpu_parallel:
+        if procs > 1 and not args.no_cpu_parallel and world == 1:
             try:
                 pv, pdesc = oracle_parallel_run(tensors, args.dtype, args.seed, min(args.cpu_budget_s, 10.0), procs)
                 line["cpu_baseline_all_cores"] = {"value": pv, "unit": "Gparams/s", "cores": procs, "kind": "oracle",
@@ -547,6 +633,82 @@ def main():
     if world > 1:
         barrier()
         dist.destroy_process_group()
+
+
+def run_e2e(args, eng, grad_buf, grads, tensors, stream, dev, psi_total, ms, barrier):
+    """Every step copies that step's gradients H2D from pinned host memory and reads the
+    step record D2H.  The copy of step s+1 (copy stream, second device buffer) overlaps
+    step s; the host reads step s's record before issuing step s+2."""
+    import torch
+    import synth
+    nb = eng.info.n_buckets
+    host = torch.empty(grad_buf.numel(), dtype=grad_buf.dtype, pin_memory=True)
+    host.copy_(grad_buf)
+    bufs = [grad_buf, torch.empty_like(grad_buf)]
+    views = [grads, [bufs[1][o:o + t.numel] for t, o in zip(tensors, synth.tensor_offsets(tensors))]]
+    copy_stream = torch.cuda.Stream(dev)
+    copied = [torch.cuda.Event(), torch.cuda.Event()]
+    consumed = [torch.cuda.Event(), torch.cuda.Event()]
+    rec = eng._info_host
+    torch.cuda.synchronize()
+    # the PCIe bound of this leg: one pinned H2D of the step's gradients, alone
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(copy_stream):
+        h0.record(copy_stream)
+        bufs[1].copy_(host, non_blocking=True)
+        h1.record(copy_stream)
+    torch.cuda.synchronize()
+    h2d_ms = h0.elapsed_time(h1)
+    barrier()
+    K = args.e2e_steps
+    layer_ids = sorted({b.layer for b in eng.buckets})
+    layer_buckets = {L: [k for k, b in enumerate(eng.buckets) if b.layer == L] for L in layer_ids}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(copy_stream)
+    with torch.cuda.stream(copy_stream):
+        bufs[0].copy_(host, non_blocking=True)
+        copied[0].record(copy_stream)
+    for s in range(K):
+        cur = s % 2
+        stream.wait_event(copied[cur])
+        eng.set_grads(views[cur])
+        if args.stage == 3:
+            for L in layer_ids:
+                eng.gather_params(L)
+                eng.release_params(L)
+            for L in reversed(layer_ids):
+                eng.gather_params(L)
+                for k in reversed(layer_buckets[L]):
+                    eng.reduce_grads(k)
+                eng.release_params(L)
+        else:
+            for k in reversed(range(nb)):
+                eng.reduce_grads(k)
+        eng.step()                              # + 32-byte step record D2H into pinned memory
+        consumed[cur].record(stream)            # joined: the flattens have read bufs[cur]
+        if s + 1 < K:
+            nxt = (s + 1) % 2
+            copy_stream.wait_event(consumed[nxt])
+            with torch.cuda.stream(copy_stream):
+                bufs[nxt].copy_(host, non_blocking=True)
+                copied[nxt].record(copy_stream)
+        stream.synchronize()                    # the host reads step s's result
+        _ = bytes(rec.numpy()[:32])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / K, dev)
+    e2e_dev_ms = max_over_ranks(e0.elapsed_time(e1) / K, dev)
+    eng.set_grads(grads)
+    del host, bufs
+    nbytes = int(grad_buf.numel() * grad_buf.element_size())
+    return {"value": psi_total / (e2e_ms * 1e-3) / 1e9, "unit": "Gparams/s",
+            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 32, "ms_per_step": e2e_ms, "steps": K,
+            "device_ms_per_step": e2e_dev_ms, "h2d_alone_ms": h2d_ms,
+            "h2d_gbs": nbytes / (h2d_ms * 1e-3) / 1e9,
+            "frac_of_h2d_bound": max(h2d_ms, ms) / e2e_ms,
+            "note": "value from the host wall clock (device_ms_per_step: CUDA events from the first H2D "
+                    "to the last step's end); H2D of step s+1 overlaps step s (double-buffered)"}
 
 
 if __name__ == "__main__":

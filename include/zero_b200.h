@@ -37,7 +37,8 @@
 extern "C" {
 #endif
 
-#define ZERO_ABI_VERSION 2     /* 2: zero_config.mp_rank, zero_tensor.flags, zero_step_begin/end, zero_pa_* */
+#define ZERO_ABI_VERSION 3     /* 2: zero_config.mp_rank, zero_tensor.flags, zero_step_begin/end, zero_pa_*;
+                                  3: zero_timing.ag_ms, R32 over NCCL, zero_wait (NCCL watchdog) */
 #define ZERO_MAX_RANKS 8      /* one NVL8 box */
 
 typedef enum {
@@ -369,6 +370,8 @@ typedef struct {          /* device time per phase, CUDA events on the launching
   double reduce_ms;       /* first flatten of a step -> last reduce-scatter/epilogue issued */
   double adam_ms;         /* the fused Adam kernel (sum over steps) */
   double step_ms;         /* zero_step: decision + Adam + all-gather */
+  double ag_ms;           /* the all-gather after the Adam kernel (NCCL transport; ~0 when the
+                             all-gather is fused into the Adam kernel's stores, PEER) */
   uint64_t steps;         /* steps accumulated */
   uint64_t kernel_launches;  /* library kernels launched (all, cumulative, never reset) */
   uint64_t adam_launches;

@@ -260,7 +260,7 @@ struct zero_ctx {
   }
 
   // phase timing (cfg.timing): one event set per step, reused from a pool
-  struct StepEvents { cudaEvent_t r0 = nullptr, r1 = nullptr, a0 = nullptr, a1 = nullptr, s1 = nullptr; };
+  struct StepEvents { cudaEvent_t r0 = nullptr, r1 = nullptr, a0 = nullptr, a1 = nullptr, g1 = nullptr, s1 = nullptr; };
   std::vector<StepEvents> ev_pool;
   size_t ev_used = 0;
   bool step_open = false;          // a reduce phase began (r0 recorded)
@@ -307,6 +307,7 @@ zero_status zero_ctx::timing_events(StepEvents** out) {
     CK0(cudaEventCreate(&e.r1));
     CK0(cudaEventCreate(&e.a0));
     CK0(cudaEventCreate(&e.a1));
+    CK0(cudaEventCreate(&e.g1));
     CK0(cudaEventCreate(&e.s1));
     ev_pool.push_back(e);
   }
@@ -1288,6 +1289,7 @@ zero_status step_finish(zero_ctx* c, const PartialPtrs& pp, zero_ctx::StepEvents
   } else if (c->transport == ZERO_TRANSPORT_PEER && (c->stage == 1 || c->stage == 2)) {
     for (uint32_t k = 0; k < c->info.n_buckets; ++k) c->counters.all_gather += c->slice(k) * (uint64_t)(c->n_d - 1);
   }
+  if (ev) CK(cudaEventRecord(ev->g1, c->comm_stream));   // end of the separate all-gather (NCCL)
   if (c->ipc) {  // the replicas (stages 1/2) / shards (stage 3) are final on every rank
     SigArgs sa{};
     for (int j = 0; j < c->n_d; ++j) sa.dst[j] = c->sig(j, c->off_sig_adam, c->rank);
@@ -1752,12 +1754,14 @@ zero_status zero_query(const zero_ctx* cc, int what, void* out, size_t n) {
         CK(cudaStreamSynchronize(c->comm_stream));
         CK(cudaStreamSynchronize(c->stream));
         for (size_t i = 0; i < c->ev_used; ++i) {
-          float a = 0, b = 0, d = 0;
+          float a = 0, b = 0, d = 0, g = 0;
           CK(cudaEventElapsedTime(&a, c->ev_pool[i].r0, c->ev_pool[i].r1));
           CK(cudaEventElapsedTime(&b, c->ev_pool[i].a0, c->ev_pool[i].a1));
+          CK(cudaEventElapsedTime(&g, c->ev_pool[i].a1, c->ev_pool[i].g1));
           CK(cudaEventElapsedTime(&d, c->ev_pool[i].r1, c->ev_pool[i].s1));
           tm.reduce_ms += a;
           tm.adam_ms += b;
+          tm.ag_ms += g;
           tm.step_ms += d;
         }
         tm.steps = c->ev_used;
@@ -1803,6 +1807,7 @@ void zero_destroy(zero_ctx* c) {
     cudaEventDestroy(e.r1);
     cudaEventDestroy(e.a0);
     cudaEventDestroy(e.a1);
+    cudaEventDestroy(e.g1);
     cudaEventDestroy(e.s1);
   }
   for (auto& gs : c->gslots) {

@@ -22,7 +22,7 @@ _LIB_PATH = os.environ.get("ZERO_LIB_PATH") or os.path.join(_PKG, "libzero_b200.
 # ---------------------------------------------------------------------------
 # ABI structs (mirror include/zero_b200.h field by field)
 # ---------------------------------------------------------------------------
-ABI_VERSION = 2           # include/zero_b200.h ZERO_ABI_VERSION
+ABI_VERSION = 3           # include/zero_b200.h ZERO_ABI_VERSION
 FP16, BF16, FP32 = 0, 1, 2
 MP_REPLICATED = 1          # zero_tensor.flags: replicated across the MP group (reading R-MP1)
 R16, R32 = 0, 1
@@ -92,7 +92,7 @@ class CComm(C.Structure):
 
 class CTiming(C.Structure):
     _fields_ = [("reduce_ms", C.c_double), ("adam_ms", C.c_double), ("step_ms", C.c_double),
-                ("steps", C.c_uint64), ("kernel_launches", C.c_uint64), ("adam_launches", C.c_uint64)]
+                ("ag_ms", C.c_double), ("steps", C.c_uint64), ("kernel_launches", C.c_uint64), ("adam_launches", C.c_uint64)]
 
 
 class CDeviceState(C.Structure):

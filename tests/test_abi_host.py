@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(z):
     dyn = subprocess.run(["nm", "-D", "--defined-only", _LIB_PATH], capture_output=True, text=True).stdout
     for n in names:
         assert re.search(rf"\bT {n}\b", dyn), n
-    assert z.zero.lib.zero_abi_version() == 2
+    assert z.zero.lib.zero_abi_version() == z.zero.ABI_VERSION == 3
 
 
 def test_library_built_for_sm100a():
