@@ -48,7 +48,8 @@ typedef enum {
   ZERO_ECUDA = 3,
   ZERO_ENCCL = 4,
   ZERO_ESTATE = 5,
-  ZERO_EUNSUPPORTED = 6
+  ZERO_EUNSUPPORTED = 6,
+  ZERO_ETIMEOUT = 7          /* zero_wait: work still running at the deadline (not sticky) */
 } zero_status;
 
 /* 16-bit model dtypes (fp16 params/grads, fp32 optimizer states). */
@@ -191,8 +192,12 @@ struct zero_ctx;
  *  (the host layout and arena sizes are usable without a GPU); the context owns only
  *  host memory until zero_bind_buffers.
  *  Errors: ZERO_EINVAL (K != 12, stage not in 0..3, bad dtype combination,
- *  rank/n_d/transport mismatch, layout errors), ZERO_EUNSUPPORTED (R32 with the
- *  NCCL transport, stage 0 with R32), ZERO_ECUDA. */
+ *  rank/n_d/transport mismatch, layout errors), ZERO_EUNSUPPORTED (stage 0 with R32;
+ *  R32 over NCCL at stage 1), ZERO_ECUDA.
+ *  R32 over NCCL (stages 2/3; also on a 1-rank communicator): each bucket is flattened
+ *  into an fp32 pool slot holding the cast/prescaled 16-bit values widened, and
+ *  reduce-scattered in fp32 (2x the 16-bit wire bytes), so no partial sum is rounded
+ *  to 16-bit; the sum order is NCCL's (exact for N_d <= 2). */
 zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage, int K,
                       const zero_config* cfg, zero_transport transport, void* nccl_comm,
                       void* compute_stream, struct zero_ctx** out);
@@ -382,6 +387,19 @@ zero_status zero_query(const struct zero_ctx* ctx, int what, void* out, size_t o
  * zero_plan_layout).  The string is owned by the library and valid until the next
  * call on the same context. */
 const char* zero_last_error(const struct zero_ctx* ctx);
+
+/* Failure detection (a transport failure is an error naming the rank, not a
+ * hang).  Blocks the host until every piece of work the context has issued so far (the
+ * caller's stream and the library's streams) has completed, or timeout_ms elapsed.
+ * NCCL transport: while waiting (and at the start of every NCCL-issuing call) the
+ * communicator's asynchronous error is polled (ncclCommGetAsyncError); on an error, or
+ * at the deadline with work outstanding, the communicator is aborted (ncclCommAbort --
+ * the only way to release a hung collective; the borrowed communicator must then be
+ * treated as destroyed by its owner) and the context is poisoned with a sticky
+ * ZERO_ENCCL whose text names this rank.  Other transports: ZERO_ETIMEOUT at the
+ * deadline (not sticky; the cross-process PEER spin-waits also trap after 300 s).
+ * Errors: ZERO_ESTATE (not bound), ZERO_ECUDA (a device error surfaced). */
+zero_status zero_wait(struct zero_ctx* ctx, uint64_t timeout_ms);
 /* Synchronize the context's streams, close IPC mappings, destroy the library's
  * streams and events and free the context.  The caller's arenas are not freed.
  * Destroying one member of a simulated group dissolves the group. */

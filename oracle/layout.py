@@ -143,15 +143,3 @@ def make_layout(numels: Sequence[int], layers: Sequence[int], n_d: int, align: i
         shard_off += b.size // n_d
     return Layout(n_d=n_d, align=align, cap=cap or 0, buckets=buckets,
                   psi=sum(numels), psi_padded=base)
-
-
-def layer_ranges(layout: Layout):
-    """layer -> (first bucket, last bucket + 1, flat start, flat end)."""
-    out = {}
-    for k, b in enumerate(layout.buckets):
-        if b.layer not in out:
-            out[b.layer] = [k, k + 1, b.base, b.base + b.size]
-        else:
-            out[b.layer][1] = k + 1
-            out[b.layer][3] = b.base + b.size
-    return {L: tuple(v) for L, v in out.items()}

@@ -11,7 +11,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <dlfcn.h>
+#include <chrono>
 #include <cstring>
+#include <thread>
 #include <map>
 #include <string>
 #include <vector>
@@ -159,7 +161,8 @@ struct zero_ctx {
   cudaStream_t comm_stream = nullptr;  // library stream for NCCL work
   bool own_comm_stream = false;
   int pdt = DT_BF16, gdt = DT_BF16;
-  bool r32 = false;                    // reduced gradient kept in fp32 (R32 and N_d > 1)
+  bool r32 = false;                    // reduced gradient kept in fp32 (R32 and N_d > 1, or NCCL)
+  bool wide = false;                   // R32 over NCCL: buckets flattened to fp32 (the RS sums fp32)
 
   // layout
   std::vector<zero_tensor> tensors;
@@ -269,6 +272,8 @@ struct zero_ctx {
 
   zero_status sticky = ZERO_OK;
   std::string err;
+  bool comm_aborted = false;                       // the NCCL watchdog aborted the communicator
+  cudaEvent_t ev_wait[kMaxFlatStreams + 2] = {};   // zero_wait: one per stream the context uses
 
   zero_status fail(zero_status s, const char* fmt, ...) {
     char buf[512];
@@ -288,6 +293,10 @@ struct zero_ctx {
     if (stage <= 1) return grad + b.base;
     if (transport == ZERO_TRANSPORT_LOCAL) return reinterpret_cast<uint16_t*>(gred) + b.shard_off;
     return grad + (uint64_t)(k % pool) * maxB;
+  }
+  void* flat_dst_any(uint32_t k) const {       // as flat_dst; fp32 pool slots for R32 over NCCL
+    if (wide) return reinterpret_cast<float*>(grad) + (uint64_t)(k % pool) * maxB;
+    return flat_dst(k);
   }
   // where bucket k's reduced slice (this rank's) lives
   void* rs_dst(uint32_t k) const {
@@ -344,6 +353,30 @@ namespace {
   } while (0)
 
 ncclDataType_t nccl_dt(int dt) { return dt == DT_F16 ? ncclFloat16 : dt == DT_BF16 ? ncclBfloat16 : ncclFloat32; }
+
+// NCCL failure handling ("transport failure -> protocol error with rank id"):
+// a failed or hung collective is unblocked only by aborting its communicator, after which
+// the context is poisoned with a sticky ZERO_ENCCL naming this rank
+zero_status abort_comm(zero_ctx* c, const char* why) {
+  if (c->comm && !c->comm_aborted) {
+    ncclCommAbort(c->comm);
+    c->comm_aborted = true;
+  }
+  return c->fail(ZERO_ENCCL, "rank %d of %d: %s; the communicator was aborted", c->rank, c->n_d, why);
+}
+// cheap host-side poll of the communicator's asynchronous error (every NCCL-issuing call)
+zero_status poll_nccl(zero_ctx* c) {
+  if (c->transport != ZERO_TRANSPORT_NCCL || !c->comm || c->comm_aborted) return ZERO_OK;
+  ncclResult_t ae = ncclSuccess;
+  const ncclResult_t r = ncclCommGetAsyncError(c->comm, &ae);
+  if (r != ncclSuccess) ae = r;
+  if (ae != ncclSuccess && ae != ncclInProgress) {
+    char why[160];
+    snprintf(why, sizeof(why), "asynchronous NCCL error: %s", ncclGetErrorString(ae));
+    return abort_comm(c, why);
+  }
+  return ZERO_OK;
+}
 
 int grid_for(uint64_t work_items, int per_sm, int sms) {
   const uint64_t cap = (uint64_t)per_sm * sms;
@@ -467,9 +500,14 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
   if (transport == ZERO_TRANSPORT_NCCL && !nccl_comm) return bad("NCCL transport requires a communicator");
   if (transport != ZERO_TRANSPORT_LOCAL && transport != ZERO_TRANSPORT_NCCL && transport != ZERO_TRANSPORT_PEER)
     return bad("unknown transport");
-  const bool r32 = cfg->reduce_mode == ZERO_R32 && n_d > 1;
-  if (r32 && transport == ZERO_TRANSPORT_NCCL) { g_init_error = "R32 is implemented on the PEER transport only"; return ZERO_EUNSUPPORTED; }
+  // R32 at N_d = 1 is R16 (one value rounded to 16-bit is itself), except on a 1-rank NCCL
+  // communicator, which keeps the fp32 collective path so that it can be tested on one GPU
+  const bool r32 = cfg->reduce_mode == ZERO_R32 && (n_d > 1 || transport == ZERO_TRANSPORT_NCCL);
   if (r32 && stage == 0) { g_init_error = "stage 0 supports R16 only"; return ZERO_EUNSUPPORTED; }
+  if (r32 && transport == ZERO_TRANSPORT_NCCL && stage == 1) {
+    g_init_error = "R32 over NCCL needs stage 2 or 3 (fp32 staging pool); stage 1 reduces in place in its 16-bit buffer";
+    return ZERO_EUNSUPPORTED;
+  }
 
   LayoutResult L;
   if (!plan(desc, n_d, L)) return bad(L.error.c_str());
@@ -490,6 +528,7 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
   c->pdt = to_dt(cfg->param_dtype);
   c->gdt = to_dt(cfg->grad_dtype);
   c->r32 = r32;
+  c->wide = r32 && c->transport == ZERO_TRANSPORT_NCCL;
   c->tensors.assign(desc->tensors, desc->tensors + desc->n_tensors);
   c->buckets = L.buckets;
   c->pieces = L.pieces;
@@ -582,7 +621,7 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
   z.opt_stride_elems = c->opt_stride;
   z.p16_bytes = 2ull * (stage == 3 ? S : P);
   if (stage <= 1) z.grad_bytes = 2ull * P;
-  else z.grad_bytes = coll ? 2ull * c->pool * c->maxB : 0;
+  else z.grad_bytes = coll ? (c->wide ? 4ull : 2ull) * c->pool * c->maxB : 0;
   if (stage >= 2) z.gred_bytes = (r32 ? 4ull : 2ull) * S;
   else z.gred_bytes = r32 ? 4ull * S : 0;
   z.gather_bytes = (stage == 3 && coll) ? 2ull * (c->cfg.prefetch_depth + 1) * c->max_layer : 0;
@@ -867,7 +906,7 @@ namespace {
 // issue the flatten of bucket k (compute stream).  epilogue at N_d == 1.
 zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads, cudaStream_t fs, GridPartials* part) {
   const auto& tmpl = c->flat_tmpl[k];
-  uint16_t* dst = c->flat_dst(k);
+  void* dst = c->flat_dst_any(k);
   const int ebytes = c->gdt == DT_F32 ? 4 : 2;
   const bool epi = c->transport == ZERO_TRANSPORT_LOCAL;
   int slot = c->slot_base[k];
@@ -889,7 +928,7 @@ zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads, cud
     a.n_pieces = (int)(b1 - b0);
     const uint64_t total = tmpl[b1 - 1].dst_off + tmpl[b1 - 1].count - tmpl[b0].dst_off;
     // TMA staging needs 16-B granules: every piece boundary and source % 8 elements
-    bool tma_ok = c->flat_tma > 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+    bool tma_ok = c->flat_tma > 0 && !c->wide && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
     for (int j = 0; tma_ok && j < (int)(b1 - b0); ++j) {
       const FlatPiece& fp = a.pieces[j];
       if ((fp.dst_off | fp.count) & 7) tma_ok = false;
@@ -912,7 +951,8 @@ zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads, cud
     }
     // chain behind the previous launch of this step's reduce phase on the same stream
     a.pdl = (c->flat_pdl && (c->n_reduced > 0 || b0 > 0)) ? 1 : 0;
-    if (tma_ok) CK(launch_flatten_tma(a, grid, fs, c->flat_tma));
+    if (c->wide) CK(launch_flatten_wide(a, grid, fs));
+    else if (tma_ok) CK(launch_flatten_tma(a, grid, fs, c->flat_tma));
     else CK(launch_flatten(a, grid, fs, c->flat_vecs));
     c->launches++;
   }
@@ -953,6 +993,7 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
   STICKY(c);
   NvtxRange nvtx("zero_reduce_grads");
   if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
+  if (zero_status ps = poll_nccl(c)) return ps;
   if (k >= c->info.n_buckets) return c->fail(ZERO_EINVAL, "bucket %u out of range", k);
   if (c->reduced[k]) return c->fail(ZERO_ESTATE, "bucket %u already reduced this step", k);
   if (c->transport == ZERO_TRANSPORT_PEER && !c->group && !c->ipc)
@@ -1099,12 +1140,13 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
   CK(cudaStreamWaitEvent(c->comm_stream, c->ev_flat, 0));
   const zero_bucket& b = c->buckets[k];
   const uint64_t sl = c->slice(k);
-  const ncclDataType_t dt = nccl_dt(c->pdt);
+  const ncclDataType_t dt = c->wide ? ncclFloat32 : nccl_dt(c->pdt);
   if (c->stage == 0) {
     NK(ncclAllReduce(c->grad + b.base, c->grad + b.base, b.size, dt, ncclSum, c->comm, c->comm_stream));
     c->counters.all_reduce += 2 * sl * (uint64_t)(c->n_d - 1);
   } else {
-    NK(ncclReduceScatter(c->flat_dst(k), c->rs_dst(k), sl, dt, ncclSum, c->comm, c->comm_stream));
+    // R16: 16-bit wire, NCCL rounds partial sums to 16-bit; R32: fp32 wire (2x bytes), fp32 sums
+    NK(ncclReduceScatter(c->flat_dst_any(k), c->rs_dst(k), sl, dt, ncclSum, c->comm, c->comm_stream));
     c->counters.reduce_scatter += sl * (uint64_t)(c->n_d - 1);
   }
   RSArgs a{};
@@ -1112,7 +1154,7 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
   a.count = sl;
   a.n = c->n_d;
   a.dtype = c->pdt;
-  a.r32 = 0;
+  a.r32 = c->r32 ? 1 : 0;
   a.reduce = 0;
   a.st = c->st;
   a.part = c->part_comm;
@@ -1199,6 +1241,7 @@ namespace {
 // per-rank {sum of squares, overflow} partials, exchanged across the data-parallel group)
 zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev) {
   if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
+  if (zero_status ps = poll_nccl(c)) return ps;
   if (c->step_begun) return c->fail(ZERO_ESTATE, "zero_step_begin already issued: finish with zero_step_end");
   ZeroGroup* g = c->group;
   if (g) {
@@ -1620,6 +1663,7 @@ zero_status zero_gather_params(zero_ctx* c, uint32_t layer, void** views_out) {
   if (c->stage != 3) return c->fail(ZERO_ESTATE, "zero_gather_params needs stage 3");
   auto it = c->layer_index.find(layer);
   if (it == c->layer_index.end()) return c->fail(ZERO_EINVAL, "unknown layer %u", layer);
+  if (zero_status ps = poll_nccl(c)) return ps;
   const int li = it->second;
   uint16_t* base;
   if (c->transport == ZERO_TRANSPORT_LOCAL) {
@@ -1783,6 +1827,45 @@ zero_status zero_query(const zero_ctx* cc, int what, void* out, size_t n) {
   }
 }
 
+zero_status zero_wait(zero_ctx* c, uint64_t timeout_ms) {
+  STICKY(c);
+  if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
+  cudaStream_t ss[zero_ctx::kMaxFlatStreams + 2];
+  int ns = 0;
+  ss[ns++] = c->stream;
+  if (c->comm_stream && c->comm_stream != c->stream) ss[ns++] = c->comm_stream;
+  for (int i = 0; i < zero_ctx::kMaxFlatStreams; ++i)
+    if (c->flat_stream[i]) ss[ns++] = c->flat_stream[i];
+  for (int i = 0; i < ns; ++i) {
+    if (!c->ev_wait[i]) CK(cudaEventCreateWithFlags(&c->ev_wait[i], cudaEventDisableTiming));
+    CK(cudaEventRecord(c->ev_wait[i], ss[i]));
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    bool done = true;
+    for (int i = 0; i < ns; ++i) {
+      const cudaError_t q = cudaEventQuery(c->ev_wait[i]);
+      if (q == cudaErrorNotReady) { done = false; continue; }
+      if (q != cudaSuccess) return c->fail(ZERO_ECUDA, "zero_wait: %s", cudaGetErrorString(q));
+    }
+    if (zero_status ps = poll_nccl(c)) return ps;
+    if (done) return ZERO_OK;
+    const uint64_t el =
+        (uint64_t)std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+    if (el >= timeout_ms) {
+      if (c->transport == ZERO_TRANSPORT_NCCL) {
+        char why[160];
+        snprintf(why, sizeof(why), "work issued by the context did not complete within %llu ms",
+                 (unsigned long long)timeout_ms);
+        return abort_comm(c, why);
+      }
+      c->err = "zero_wait: device work did not complete within " + std::to_string(timeout_ms) + " ms";
+      return ZERO_ETIMEOUT;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+}
+
 const char* zero_last_error(const zero_ctx* c) {
   if (!c) return g_init_error.c_str();
   return c->err.c_str();
@@ -1822,6 +1905,7 @@ void zero_destroy(zero_ctx* c) {
     if (c->ev_join[i]) cudaEventDestroy(c->ev_join[i]);
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  for (auto& e : c->ev_wait) if (e) cudaEventDestroy(e);
   if (c->ev_flat) cudaEventDestroy(c->ev_flat);
   if (c->ev_step) cudaEventDestroy(c->ev_step);
   if (c->own_comm_stream && c->comm_stream) cudaStreamDestroy(c->comm_stream);

@@ -505,6 +505,70 @@ cudaError_t launch_flatten_v(const FlatArgs& a, int grid, cudaStream_t s) {
 }
 
 
+// ---------------------------------------------------------------------------
+// K2 (fp32 bucket, R32 over NCCL): the same cast/prescale -- g' = RTNE16(widen(g) *
+// sigma), the 16-bit value the oracle sums (c-2) -- stored widened to fp32, so that
+// ncclReduceScatter sums fp32 values and no partial sum is rounded to 16-bit on the
+// wire.  No epilogue: the flag and norm are taken after the reduction.
+// ---------------------------------------------------------------------------
+template <int SDT, int DDT>
+__global__ void __launch_bounds__(kThreads) k_flatten_wide(const __grid_constant__ FlatArgs a) {
+  using S = SrcLoad<SDT>;
+  using D = H16<DDT>;
+  const bool copy = a.sigma == 1.0f && SDT == DDT;
+  float* dst_base = reinterpret_cast<float*>(a.dst);
+  const uint64_t r0 = a.pieces[0].dst_off;
+  const uint64_t r1 = a.pieces[a.n_pieces - 1].dst_off + a.pieces[a.n_pieces - 1].count;
+  const uint64_t lo = r0 + (uint64_t)blockIdx.x * a.per_cta;
+  const uint64_t hi = lo + a.per_cta < r1 ? lo + a.per_cta : r1;
+  int p = 0;
+  while (p + 1 < a.n_pieces && a.pieces[p + 1].dst_off <= lo) ++p;
+  for (uint64_t cur = lo; cur < hi && p < a.n_pieces; ++p) {
+    const FlatPiece pc = a.pieces[p];
+    const uint64_t pend = pc.dst_off + pc.count < hi ? pc.dst_off + pc.count : hi;
+    if (pend <= cur) continue;
+    float* dst = dst_base + cur;
+    const uint32_t n = (uint32_t)(pend - cur);
+    if (pc.src == nullptr) {  // alignment gap or padding: zeros (reading c-7)
+      for (uint32_t i = threadIdx.x; i < n; i += kThreads) dst[i] = 0.0f;
+      cur = pend;
+      continue;
+    }
+    const char* src = reinterpret_cast<const char*>(pc.src) + (cur - pc.dst_off) * S::kBytes;
+    auto cast1 = [&](float x) { return D::widen(copy ? D::narrow(x) : D::narrow(__fmul_rn(x, a.sigma))); };
+    if (aligned(src, 8 * S::kBytes) && aligned(dst, 32)) {
+      const uint32_t nv = n & ~7u;
+      for (uint32_t i = threadIdx.x * 8; i < nv; i += kThreads * 8) {
+        float x[8];
+        S::vec(src + (uint64_t)i * S::kBytes, x);
+        U8 o;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o.x[j] = __float_as_uint(cast1(x[j]));
+        st256(dst + i, o);
+      }
+      for (uint32_t j = nv + threadIdx.x; j < n; j += kThreads) dst[j] = cast1(S::one(src, j));
+    } else {
+      for (uint32_t j = threadIdx.x; j < n; j += kThreads) dst[j] = cast1(S::one(src, j));
+    }
+    cur = pend;
+  }
+}
+
+cudaError_t launch_flatten_wide(const FlatArgs& a, int grid, cudaStream_t s) {
+  if (a.dst_dtype == DT_F16) {
+    if (a.src_dtype == DT_F16) k_flatten_wide<DT_F16, DT_F16><<<grid, kThreads, 0, s>>>(a);
+    else if (a.src_dtype == DT_F32) k_flatten_wide<DT_F32, DT_F16><<<grid, kThreads, 0, s>>>(a);
+    else return cudaErrorInvalidValue;
+  } else if (a.dst_dtype == DT_BF16) {
+    if (a.src_dtype == DT_BF16) k_flatten_wide<DT_BF16, DT_BF16><<<grid, kThreads, 0, s>>>(a);
+    else if (a.src_dtype == DT_F32) k_flatten_wide<DT_F32, DT_BF16><<<grid, kThreads, 0, s>>>(a);
+    else return cudaErrorInvalidValue;
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s, int vecs) {
   switch (vecs) {
     case 4: return launch_flatten_v<4>(a, grid, s);

@@ -157,6 +157,8 @@ struct ShardIOArgs {           // checkpoint: per-tensor fp32 piece <-> owned sh
 // launchers (kernels.cu); return the launch error
 cudaError_t launch_flatten(const FlatArgs& a, int grid, cudaStream_t s, int vecs);
 cudaError_t launch_flatten_tma(const FlatArgs& a, int grid, cudaStream_t s, int variant);
+// the cast/prescaled 16-bit values stored widened to fp32 (R32 over NCCL); no epilogue
+cudaError_t launch_flatten_wide(const FlatArgs& a, int grid, cudaStream_t s);
 int flatten_tma_ctas_per_sm(int variant);
 cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s);
 // cta_*: optional per-CTA flatten partials (N_d == 1), slot i at [i * kMaxGrid, + cta_grid[i])

@@ -28,7 +28,7 @@ MP_REPLICATED = 1          # zero_tensor.flags: replicated across the MP group (
 R16, R32 = 0, 1
 TRANSPORT = {"local": 0, "nccl": 1, "peer": 2}
 STATUS = {0: "ZERO_OK", 1: "ZERO_EINVAL", 2: "ZERO_ENOMEM", 3: "ZERO_ECUDA", 4: "ZERO_ENCCL",
-          5: "ZERO_ESTATE", 6: "ZERO_EUNSUPPORTED"}
+          5: "ZERO_ESTATE", 6: "ZERO_EUNSUPPORTED", 7: "ZERO_ETIMEOUT"}
 Q_LAYOUT, Q_MEMORY, Q_COMM, Q_STEP, Q_BUCKETS, Q_PIECES, Q_STATE, Q_TIMING, Q_DECISION = range(9)
 
 
@@ -104,7 +104,7 @@ EXPORTS = ["zero_plan_layout", "zero_init", "zero_buffer_sizes", "zero_bind_buff
            "zero_peer_export", "zero_peer_open", "zero_export_state", "zero_import_state",
            "zero_load_master", "zero_set_grad_ptrs", "zero_reduce_grads", "zero_step", "zero_step_begin",
            "zero_step_end", "zero_gather_params",
-           "zero_release_params", "zero_param_view", "zero_query", "zero_last_error", "zero_destroy",
+           "zero_release_params", "zero_param_view", "zero_query", "zero_last_error", "zero_wait", "zero_destroy",
            "zero_model_state_bytes", "zero_comm_elems_per_rank", "zero_abi_version",
            "zero_pa_init", "zero_pa_get_info", "zero_pa_bind", "zero_pa_sim_group", "zero_pa_save",
            "zero_pa_prefetch", "zero_pa_gather", "zero_pa_get_counters", "zero_pa_last_error", "zero_pa_destroy",
@@ -140,6 +140,7 @@ def _load():
         "zero_param_view": ([P, C.c_uint32, C.POINTER(P)], C.c_int),
         "zero_query": ([P, C.c_int, P, C.c_size_t], C.c_int),
         "zero_last_error": ([P], C.c_char_p),
+        "zero_wait": ([P, C.c_uint64], C.c_int),
         "zero_destroy": ([P], None),
         "zero_model_state_bytes": ([C.c_uint64, C.c_int, C.c_int, C.c_int], C.c_uint64),
         "zero_comm_elems_per_rank": ([C.c_uint64, C.c_int, C.c_int], C.c_uint64),
@@ -395,6 +396,11 @@ class ZeroEngine:
         scratch = self.arenas["scratch"]
         off = ptr.value - scratch.data_ptr()
         return scratch[off:off + 16].view(torch.float64)
+
+    def wait(self, timeout_ms: int = 600000):
+        """zero_wait: block until the context's work completed; NCCL failures and hangs
+        abort the communicator and raise ZeroError (ZERO_ENCCL, naming the rank)."""
+        _check(lib.zero_wait(self._ctx, int(timeout_ms)), self._ctx)
 
     def step_info(self) -> CStepInfo:
         """The last step's record (synchronizes the device)."""

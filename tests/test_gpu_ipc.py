@@ -23,7 +23,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, stage, dt, mode, q):
+def _worker(rank, world, port, stage, dt, mode, q, distinct=False):
     import sys
     import traceback
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -38,7 +38,7 @@ def _worker(rank, world, port, stage, dt, mode, q):
         from paper_1910_02054_b200 import ZeroEngine
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(rank if distinct else 0)   # distinct: one GPU per rank (NVLink)
         ts = synth.mlp_layout((120, 90, 60, 30))
         nl, ll = [t.numel for t in ts], [t.layer for t in ts]
         cfg = OS.AdamConfig.defaults(dt, reduce_mode=mode)
@@ -104,6 +104,30 @@ def _worker(rank, world, port, stage, dt, mode, q):
         raise
 
 
+def run_workers(target, world, pre=(), post=(), timeout=300):
+    """Start `world` spawned processes target(rank, world, port, *pre, q, *post); return the
+    queue messages (asserting none hung and every exit code is 0)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _port()
+    procs = [ctx.Process(target=target, args=(r, world, port) + tuple(pre) + (q,) + tuple(post))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout)
+    hung = [p for p in procs if p.is_alive()]
+    for p in hung:
+        p.kill()
+        p.join(10)
+    msgs = []
+    while not q.empty():
+        msgs.append(q.get())
+    assert not hung, f"workers hung: {msgs}"
+    assert all(p.exitcode == 0 for p in procs), msgs
+    return msgs
+
+
 @pytest.mark.parametrize("world,stage,dt,mode", [(2, 1, "bf16", "R16"), (2, 2, "fp16", "R16"), (2, 3, "bf16", "R16"),
                                                  (2, 0, "bf16", "R16"), (3, 2, "bf16", "R32"),
                                                  (4, 3, "fp16", "R16")])
@@ -127,7 +151,7 @@ def test_processes_share_one_gpu(world, stage, dt, mode):
     assert all(p.exitcode == 0 for p in procs) and msgs == ["ok"] * world, msgs
 
 
-def _torch_worker(rank, world, port, stage, q):
+def _torch_worker(rank, world, port, stage, q, distinct=False):
     import sys
     import traceback
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -142,7 +166,7 @@ def _torch_worker(rank, world, port, stage, q):
         from test_gpu_torch_zero import TinyGPTUntied
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(rank if distinct else 0)
         torch.manual_seed(3)                       # same initial weights on every rank
         model = TinyGPTUntied().cuda().to(torch.bfloat16)
         init = [p.detach().float().cpu().numpy().reshape(-1).copy() for p in model.parameters()]
@@ -242,7 +266,7 @@ def _handshake_worker(rank, world, port, q):
 
 def test_open_without_peer_times_out():
     """zero_peer_open's handshake is bounded: a peer that never links is reported as an
-    error within ZERO_PEER_TIMEOUT_MS (bench.py then falls back to NCCL), not a hang."""
+    error within ZERO_PEER_TIMEOUT_MS (bench.py then exits with that error), not a hang."""
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     port = _port()

@@ -60,5 +60,23 @@ def test_communication_overhead_below_ten_percent():
         assert A.megatron_block_comm(s, h) == 12 * s * h
         ratio = Fraction(A.pa_block_comm(s, h), A.megatron_block_comm(s, h))
         assert ratio == Fraction(1, 12) and ratio < Fraction(1, 10)
-    # P_a+cpu moves each rank's partition to the host and back
-    assert A.pa_cpu_extra_transfer(1024, 8192, 32, 16) == 2 * Fraction(32 * 1024 * 8192, 16)
+
+
+@pytest.mark.parametrize("n_m", [1, 2, 3, 4, 8, 16])
+def test_pa_cpu_transfer_brute_force(n_m):
+    """P_a+cpu offloads the partitioned checkpoints 'at the expense of 2x added data
+    movement to and from CPU memory compared to P_a'.  Brute force: simulate one block's
+    offload on a concrete checkpoint -- every MP rank copies its partition (the oracle's
+    `partition`, not the formula) to the host after the forward and back before the
+    recompute -- and count the elements that cross PCIe.  Summed over the MP group it is
+    twice P_a's all-gather message b*s*h, i.e. 2 x the checkpoint, and per rank
+    twice its 1/N_m share when b*s*h fills whole 16-byte granules."""
+    rng = np.random.default_rng(n_m)
+    for b, s, h in [(1, 64, 48), (2, 32, 48), (3, 16, 48)]:   # b*s*h a multiple of 8 * N_m: no padding
+        x = rng.integers(1, 1 << 16, size=b * s * h, dtype=np.uint16)
+        to_host = [A.partition(x, n_m, r) for r in range(n_m)]      # D2H after the forward
+        back = [y.copy() for y in to_host]                          # H2D before the recompute
+        moved = sum(y.size for y in to_host) + sum(y.size for y in back)
+        assert np.array_equal(A.gather(back, x.size), x)            # what comes back is the checkpoint
+        assert moved == 2 * A.pa_block_comm(s, h, b)                # 2x P_a's all-gather message (P:492, P:496)
+        assert Fraction(moved, n_m) == A.pa_cpu_extra_transfer(s, h, b, n_m)
