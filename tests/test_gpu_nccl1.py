@@ -65,3 +65,98 @@ def test_nccl_one_rank_matches_oracle(comm, dt, stage):
     c = e.comm_counters()
     assert c.steps == 5
     p.destroy()
+
+
+@pytest.mark.parametrize("dt", ["bf16", "fp16"])
+@pytest.mark.parametrize("stage", [2, 3])
+def test_nccl_r32_one_rank_matches_oracle(comm, dt, stage):
+    """R32 over NCCL: every bucket is flattened into an fp32 pool slot
+    (the cast/prescaled 16-bit values, widened) and reduce-scattered as fp32 into the fp32
+    reduced-gradient shard; the epilogue reads fp32.  On one rank the fp32 collective is an
+    identity, so the result equals the R32 oracle bit for bit."""
+    ts = synth.mlp_layout((300, 200, 100, 50))
+    cfg = OS.AdamConfig.defaults(dt, reduce_mode="R32")
+    p = Pair(Run(ts, 1, stage, cfg, cap=1 << 13, inject=(2,), transport="nccl", nccl_comm=comm))
+    e = p.engines[0]
+    maxb = max(b.size for b in e.buckets)
+    assert e.sizes.grad_bytes == 4 * 2 * maxb          # two fp32 C_B staging slots
+    assert e.sizes.gred_bytes == 4 * e.info.shard      # fp32 reduced-gradient shard
+    for s in range(5):
+        oi, gi = p.step()
+        p.compare_info(oi, gi)
+        assert oi.overflow == (s == 2)
+    p.compare()
+    p.destroy()
+
+
+def test_nccl_r32_stage1_unsupported(comm):
+    from paper_1910_02054_b200 import ZeroConfig, ZeroEngine, ZeroError
+    ts = synth.mlp_layout((64, 32))
+    with pytest.raises(ZeroError, match="EUNSUPPORTED"):
+        ZeroEngine([t.numel for t in ts], [t.layer for t in ts], 1, 0, 1, ZeroConfig(reduce_mode="R32"),
+                   transport="nccl", nccl_comm=comm)
+
+
+_WATCHDOG = r"""
+import os, sys, time
+sys.path[:0] = [{root!r}]
+import torch, torch.distributed as dist
+import synth
+from paper_1910_02054_b200 import ZeroConfig, ZeroEngine, ZeroError, nccl_comm_ptr
+os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="{port}")
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+t = torch.ones(1, device="cuda"); dist.all_reduce(t); torch.cuda.synchronize()
+ts = synth.mlp_layout((256, 128, 64))
+e = ZeroEngine([x.numel for x in ts], [x.layer for x in ts], 1, 0, 2, ZeroConfig.defaults("bf16"),
+               "nccl", nccl_comm=nccl_comm_ptr(dist.group.WORLD), bucket_cap=1 << 12)
+e.load_master(synth.gpu_masters(ts, 1, "cuda"))
+_, g = synth.gpu_grads_flat(ts, 1, 0, 0, torch.bfloat16, "cuda")
+for k in reversed(range(e.info.n_buckets)):
+    e.reduce_grads(k, g)
+e.step()
+e.wait(60000)                                   # a healthy step completes: no error
+torch.cuda._sleep(int(3e9))                     # the caller's stream stalls for ~1.5 s ...
+for k in reversed(range(e.info.n_buckets)):     # ... so the step's collectives cannot finish
+    e.reduce_grads(k, g)
+e.step()
+t0 = time.time()
+try:
+    e.wait(100)
+    print("RESULT no error"); sys.stdout.flush(); os._exit(0)
+except ZeroError as exc:
+    dt = time.time() - t0
+    msg = str(exc)
+try:
+    e.reduce_grads(0, g)
+    sticky = "not sticky"
+except ZeroError as exc2:
+    sticky = "sticky" if exc2.status == 4 else f"status {{exc2.status}}"
+print(f"RESULT {{dt:.3f}} {{sticky}} | {{msg}}"); sys.stdout.flush()
+try:
+    torch.cuda.synchronize()
+except Exception:
+    pass
+os._exit(0)
+"""
+
+
+def test_nccl_watchdog_aborts_a_stalled_step():
+    """zero_wait (a transport failure is an error naming the rank, not a hang):
+    the step's collectives are held back by a stalled stream; the host-side wait times
+    out, aborts the communicator and returns a sticky ZERO_ENCCL naming the rank.  Run in
+    a child process (the aborted communicator belongs to its torch process group)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    r = subprocess.run([sys.executable, "-c", _WATCHDOG.format(root=root, port=port)], capture_output=True,
+                       text=True, timeout=300)
+    line = [x for x in r.stdout.splitlines() if x.startswith("RESULT")]
+    assert line, r.stdout[-2000:] + r.stderr[-2000:]
+    res = line[0]
+    assert "ZERO_ENCCL" in res and "rank 0 of 1" in res and "did not complete within 100 ms" in res, res
+    assert " sticky " in res, res
+    assert float(res.split()[1]) < 2.0, res          # reported promptly, not after the stall
