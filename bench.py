@@ -411,23 +411,31 @@ def main():
         layer_ids = sorted({b.layer for b in eng.buckets})
         layer_buckets = {L: [k for k, b in enumerate(eng.buckets) if b.layer == L] for L in layer_ids}
 
-        def one_step():
+        def one_step(evs=None):
             if args.stage == 3:
                 # SURVEY §8d step-only protocol for P_os+g+p: gather every layer for the
                 # forward (prefetching the next), then in reverse for the backward, each layer
                 # followed by its buckets' reduce-scatter; release after use
+                if evs:
+                    evs[0].record(stream)
                 for L in layer_ids:
                     eng.gather_params(L)
                     eng.release_params(L)
+                if evs:
+                    evs[1].record(stream)
                 for L in reversed(layer_ids):
                     eng.gather_params(L)
                     for k in reversed(layer_buckets[L]):
                         eng.reduce_grads(k)
                     eng.release_params(L)
+                if evs:
+                    evs[2].record(stream)
             else:
                 for k in reversed(range(nb)):
                     eng.reduce_grads(k)
             eng.step()
+            if evs:
+                evs[3].record(stream)
         return one_step
 
     def timed(eng, steps, sample_clocks=True):
@@ -474,13 +482,25 @@ def main():
         clk = clocks.stop() if clocks else None
         tm = eng.timing()
         launches = tm.kernel_launches - launches0 if graph is None else launches_per_step * steps
+        phases = None
+        if args.stage == 3 and graph is None:
+            # one more (untimed) step with events on the caller's stream: with no model compute
+            # in the step-only protocol, the forward phase is the exposed gather time
+            pe = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            one_step(pe)
+            torch.cuda.synchronize()
+            phases = {"fwd_gather_phase_ms": pe[0].elapsed_time(pe[1]),
+                      "bwd_gather_reduce_phase_ms": pe[1].elapsed_time(pe[2]),
+                      "step_phase_ms": pe[2].elapsed_time(pe[3]),
+                      "note": "caller-stream events; no model compute in the step-only protocol, so the "
+                              "forward phase is all exposed gather time (a real forward hides it, P:476)"}
         rec = eng.step_info()
         if graph is None:
             sent = [(getattr(comm2, f) - getattr(comm1, f)) / steps for f in ("reduce_scatter", "all_gather", "all_reduce")]
         else:   # replays do not pass through the host counters: the captured step's counts
             sent = [getattr(comm1, f) - getattr(comm0, f) for f in ("reduce_scatter", "all_gather", "all_reduce")]
         return {"ms": ms, "per_step": per_step, "tm": tm, "launches": launches, "clocks": clk, "rec": rec,
-                "graph": graph is not None, "sent": sent}
+                "graph": graph is not None, "sent": sent, "phases": phases}
 
     eng, cfg, grad_buf, grads = build(args.dtype)
     info = eng.info
@@ -581,6 +601,7 @@ def main():
                           "reduce_phase_ms": reduce_ms, "flatten_gbs": 4 * pp / (reduce_ms * 1e-3) / 1e9
                           if (N == 1 and reduce_ms) else None},
         "comm": comm,
+        "stage3_phases": res["phases"],
         "cuda_graph": res["graph"],
         "clocks": res["clocks"],
         "gpu_launches": int(res["launches"]),

@@ -193,11 +193,14 @@ struct zero_ctx {
   uint16_t* gather = nullptr;
   DevState* st = nullptr;
   Slot* slots = nullptr;
-  double* cta_sum = nullptr;                       // LOCAL: per-CTA flatten partials per slot
+  double* cta_sum = nullptr;                       // per-CTA epilogue partials per slot (flatten at N_d = 1,
+                                                   // reduce-scatter at N_d > 1)
   uint32_t* cta_flag = nullptr;
   uint32_t* cta_grid = nullptr;
   bool flat_pdl = false;                           // ZERO_FLAT_PDL: one flatten stream, PDL-chained launches
   bool flat_cta_partials = true;                   // ZERO_FLAT_CTA_PARTIALS=0: last-CTA combine in each flatten
+  bool rs_cta_partials = true;                     // ZERO_RS_CTA_PARTIALS=0: last-CTA combine in each reduce-scatter
+  int rs_ctas = 4, rs_u = 0;                       // ZERO_RS_CTAS (CTAs per SM), ZERO_RS_U (0 = per-N default)
   // ZeRO x MP (R-MP1): per-slot norm weights (0 for MP-replicated buckets on MP rank > 0)
   double* slot_w = nullptr;
   std::vector<double> slot_w_host;
@@ -229,6 +232,12 @@ struct zero_ctx {
   int flat_vecs = 4, flat_ctas = 4;                // ZERO_FLAT_VECS / ZERO_FLAT_CTAS
   int flat_tma = 0;                                // ZERO_FLAT_TMA: 0 off, else the TMA variant
 
+  // LOCAL: adjacent small buckets are flattened by one launch, issued at the next bucket that
+  // does not join the run or at zero_step (the gradients are borrowed until zero_step anyway)
+  int pend_lo = -1, pend_hi = -1;
+  std::vector<std::pair<uint32_t, FlatPiece>> pend_pieces;  // (bucket, piece with its source resolved)
+  uint64_t small_bucket = 1ull << 20;              // ZERO_SMALL_BUCKET (elements; 0 = never batch)
+
   // per-step tracking
   std::vector<uint8_t> reduced;
   uint32_t n_reduced = 0;
@@ -239,6 +248,12 @@ struct zero_ctx {
   bool stepped_this_round = false;
 
   // stage 3
+  // cross-process PEER: layer gathers run on their own stream (pipelined, spread
+  // over the forward and backward), ordered by ev_params (the shards are final: after a
+  // load or a step's end barrier) and each slot's freed event; the caller's stream waits
+  // on the slot's ready event
+  cudaStream_t gather_stream = nullptr;
+  cudaEvent_t ev_params = nullptr, ev_gjoin = nullptr;
   std::vector<GatherSlot> gslots;
   std::vector<int> layer_slot;                     // layer index -> gather slot (-1)
   int last_layer = -1;
@@ -273,7 +288,7 @@ struct zero_ctx {
   zero_status sticky = ZERO_OK;
   std::string err;
   bool comm_aborted = false;                       // the NCCL watchdog aborted the communicator
-  cudaEvent_t ev_wait[kMaxFlatStreams + 2] = {};   // zero_wait: one per stream the context uses
+  cudaEvent_t ev_wait[kMaxFlatStreams + 3] = {};   // zero_wait: one per stream the context uses
 
   zero_status fail(zero_status s, const char* fmt, ...) {
     char buf[512];
@@ -386,6 +401,37 @@ int grid_for(uint64_t work_items, int per_sm, int sms) {
   return (int)g;
 }
 
+// the reduce-scatter's epilogue destination for bucket k (per-CTA partials or grid combine),
+// its loads-in-flight knob and its grid
+int rs_setup(const zero_ctx* c, uint32_t k, RSArgs& a, uint64_t sl) {
+  const int slot = c->slot_base[k];
+  if (c->rs_cta_partials) {
+    a.cta_sum = c->cta_sum + (size_t)slot * kMaxGrid;
+    a.cta_flag = c->cta_flag + (size_t)slot * kMaxGrid;
+    a.cta_grid = c->cta_grid + slot;
+  }
+  a.u = c->rs_u;
+  return grid_for((sl + 2047) / 2048, c->rs_ctas, c->sms);
+}
+
+DecideParams decide_params(const zero_ctx* c);
+
+// the rank's {sum of squares, overflow} partial from the per-bucket epilogue results;
+// *decided (N_d = 1, zero_step): the same launch also made the step's decision
+cudaError_t issue_decide_local(zero_ctx* c, cudaStream_t s, bool* decided = nullptr) {
+  const bool cp = c->transport == ZERO_TRANSPORT_LOCAL ? c->flat_cta_partials : c->rs_cta_partials;
+  const double* w = c->use_slot_w ? c->slot_w : nullptr;
+  c->launches++;
+  if (cp && c->n_slots <= kMaxGrid) {   // one CTA per slot, last CTA combines (part_compute is free here)
+    DecideParams p = decide_params(c);
+    if (decided) *decided = true;
+    return launch_decide_local_slots(c->n_slots, c->my_partial, s, w, c->cta_sum, c->cta_flag, c->cta_grid,
+                                     c->part_compute, decided ? c->st : nullptr, decided ? &p : nullptr);
+  }
+  return launch_decide_local(c->slots, c->n_slots, c->my_partial, s, w, cp ? c->cta_sum : nullptr,
+                             cp ? c->cta_flag : nullptr, cp ? c->cta_grid : nullptr);
+}
+
 // bytes of the scratch arena and the offsets inside it
 struct ScratchLayout {
   size_t st, slots, part_compute, part_flat2, part_flat3, part_flat4, part_comm, my_partial, gathered, segs, sig_flat, sig_rs, sig_part, sig_adam,
@@ -393,8 +439,9 @@ struct ScratchLayout {
 };
 // sig_flat[k][r] / sig_rs[k][r]: epoch at which rank r flattened / finished reducing bucket k
 // sig_part[r] / sig_adam[r]: epoch at which rank r published its partial / finished Adam
-// local: N_d == 1 -- per-CTA flatten epilogue partials for every slot (k_decide_local)
-ScratchLayout scratch_layout(int n_slots, size_t n_segs, size_t n_buckets, bool local) {
+// per-CTA epilogue partials for every slot (k_decide_local): the flatten's at N_d == 1,
+// the reduce-scatter's (first slot of each bucket) at N_d > 1
+ScratchLayout scratch_layout(int n_slots, size_t n_segs, size_t n_buckets) {
   ScratchLayout s{};
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
@@ -414,7 +461,7 @@ ScratchLayout scratch_layout(int n_slots, size_t n_segs, size_t n_buckets, bool 
   s.sig_adam = take(sizeof(uint64_t) * ZERO_MAX_RANKS);
   s.sig_hello = take(sizeof(uint64_t) * ZERO_MAX_RANKS);   // zero_peer_open's handshake
   s.hello_result = take(sizeof(uint32_t));
-  const size_t ns = local ? (size_t)std::max(n_slots, 1) : 0;
+  const size_t ns = (size_t)std::max(n_slots, 1);
   s.cta_sum = take(sizeof(double) * kMaxGrid * ns);
   s.cta_flag = take(sizeof(uint32_t) * kMaxGrid * ns);
   s.cta_grid = take(sizeof(uint32_t) * ns);
@@ -626,7 +673,7 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
   else z.gred_bytes = r32 ? 4ull * S : 0;
   z.gather_bytes = (stage == 3 && coll) ? 2ull * (c->cfg.prefetch_depth + 1) * c->max_layer : 0;
   z.scratch_bytes =
-      scratch_layout(c->n_slots, c->segs_host.size(), c->buckets.size(), c->transport == ZERO_TRANSPORT_LOCAL).total;
+      scratch_layout(c->n_slots, c->segs_host.size(), c->buckets.size()).total;
 
   c->reduced.assign(c->info.n_buckets, 0);
   c->pool_pending.assign(c->pool, -1);
@@ -666,17 +713,15 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   c->gred = b->gred;
   c->gather = reinterpret_cast<uint16_t*>(b->gather);
   const ScratchLayout sl =
-      scratch_layout(c->n_slots, c->segs_host.size(), c->buckets.size(), c->transport == ZERO_TRANSPORT_LOCAL);
+      scratch_layout(c->n_slots, c->segs_host.size(), c->buckets.size());
   char* s = reinterpret_cast<char*>(b->scratch);
   c->st = reinterpret_cast<DevState*>(s + sl.st);
   c->slots = reinterpret_cast<Slot*>(s + sl.slots);
   c->slot_w = reinterpret_cast<double*>(s + sl.slot_w);
   c->dp_partial = reinterpret_cast<RankPartial*>(s + sl.dp_partial);
-  if (c->transport == ZERO_TRANSPORT_LOCAL) {
-    c->cta_sum = reinterpret_cast<double*>(s + sl.cta_sum);
-    c->cta_flag = reinterpret_cast<uint32_t*>(s + sl.cta_flag);
-    c->cta_grid = reinterpret_cast<uint32_t*>(s + sl.cta_grid);
-  }
+  c->cta_sum = reinterpret_cast<double*>(s + sl.cta_sum);
+  c->cta_flag = reinterpret_cast<uint32_t*>(s + sl.cta_flag);
+  c->cta_grid = reinterpret_cast<uint32_t*>(s + sl.cta_grid);
   c->part_compute = reinterpret_cast<GridPartials*>(s + sl.part_compute);
   c->part_flat[0] = c->part_compute;
   c->part_flat[1] = reinterpret_cast<GridPartials*>(s + sl.part_flat2);
@@ -714,10 +759,20 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
     c->comm_stream = c->stream;
   }
   if (const char* ev = getenv("ZERO_FLAT_CTA_PARTIALS")) c->flat_cta_partials = atoi(ev) != 0;
-  if (const char* ev = getenv("ZERO_FLAT_PDL")) c->flat_pdl = atoi(ev) != 0 && c->transport == ZERO_TRANSPORT_LOCAL;
-  if (c->flat_pdl) c->n_flat_streams = 1;
+  if (const char* ev = getenv("ZERO_RS_CTA_PARTIALS")) c->rs_cta_partials = atoi(ev) != 0;
+  if (const char* ev = getenv("ZERO_RS_CTAS")) c->rs_ctas = std::max(1, std::min(8, atoi(ev)));
+  if (const char* ev = getenv("ZERO_RS_U")) c->rs_u = atoi(ev);
+  if (const char* ev = getenv("ZERO_SMALL_BUCKET")) c->small_bucket = strtoull(ev, nullptr, 10);
   if (const char* ev = getenv("ZERO_FLAT_STREAMS"))
     c->n_flat_streams = std::max(1, std::min(zero_ctx::kMaxFlatStreams, atoi(ev)));
+  if (const char* ev = getenv("ZERO_FLAT_PDL")) c->flat_pdl = atoi(ev) != 0 && c->transport == ZERO_TRANSPORT_LOCAL;
+  if (c->flat_pdl) {
+    // PDL chains the flattens on ONE stream and lets consecutive grids overlap: they must not
+    // share a last-CTA combine (grid_publish's ticket and per-CTA sums), so each launch keeps
+    // its own per-CTA partials
+    c->n_flat_streams = 1;
+    c->flat_cta_partials = true;
+  }
   c->n_flat_streams_req = c->n_flat_streams;
   // simulated PEER ranks share one stream (host-ordered collectives); zero_peer_open
   // switches a cross-process PEER context to forked flatten streams + a comm stream
@@ -727,6 +782,8 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   CK(cudaEventCreateWithFlags(&c->ev_flat, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_step, cudaEventDisableTiming));
   if (c->stage == 3) {
+    CK(cudaEventCreateWithFlags(&c->ev_params, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_gjoin, cudaEventDisableTiming));
     c->gslots.resize(c->cfg.prefetch_depth + 1);
     for (auto& g : c->gslots) {
       CK(cudaEventCreateWithFlags(&g.ready, cudaEventDisableTiming));
@@ -787,6 +844,7 @@ zero_status zero_load_master(zero_ctx* c, const void* const* tensor_master) {
   const float inv = (float)(1.0 / ((double)c->n_d * (double)c->cfg.loss_scale * (double)c->cfg.grad_prescale));
   CK(launch_init_state(c->st, c->cfg.loss_scale, inv, c->stream));
   c->launches++;
+  if (c->ev_params) CK(cudaEventRecord(c->ev_params, c->stream));   // the shards are written
   return ZERO_OK;
 }
 
@@ -889,6 +947,7 @@ zero_status zero_import_state(zero_ctx* c, const void* const* master, const void
     CK(launch_set_state(c->st, st->b1t, st->b2t, st->t, st->loss_scale, st->good_steps, inv, c->stream));
     c->launches++;
   }
+  if (c->ev_params) CK(cudaEventRecord(c->ev_params, c->stream));
   return ZERO_OK;
 }
 
@@ -959,6 +1018,98 @@ zero_status issue_flatten(zero_ctx* c, uint32_t k, const void* const* grads, cud
   return ZERO_OK;
 }
 
+// the stream a flatten is issued on: the caller's, or the next forked flatten stream
+zero_status pick_flat_stream(zero_ctx* c, cudaStream_t* fs, GridPartials** fpart) {
+  *fs = c->stream;
+  *fpart = c->part_compute;
+  if (c->n_flat_streams > 1) {
+    const int i = (int)(c->flat_rr++ % (uint32_t)c->n_flat_streams);
+    *fs = c->flat_stream[i];
+    *fpart = c->part_flat[i];
+    CK(cudaEventRecord(c->ev_fork, c->stream));
+    CK(cudaStreamWaitEvent(*fs, c->ev_fork, 0));
+    c->flat_used[i] = true;
+  }
+  return ZERO_OK;
+}
+
+bool batchable(const zero_ctx* c, uint32_t k) {
+  return c->transport == ZERO_TRANSPORT_LOCAL && c->small_bucket && c->buckets[k].size <= c->small_bucket &&
+         c->flat_tmpl[k].size() <= (size_t)kMaxFlatPieces && c->flat_cta_partials && !c->flat_pdl && !c->flat_tma &&
+         !c->use_slot_w;
+}
+
+// one launch for the pending run of adjacent small buckets [pend_lo, pend_hi] (N_d = 1): their
+// pieces tile [base_lo, base_hi + B_hi) contiguously; the epilogue partials go to the first
+// bucket's slot and the run's other slots are cleared
+zero_status flush_small(zero_ctx* c) {
+  if (c->pend_lo < 0) return ZERO_OK;
+  std::stable_sort(c->pend_pieces.begin(), c->pend_pieces.end(),
+                   [](const std::pair<uint32_t, FlatPiece>& x, const std::pair<uint32_t, FlatPiece>& y) {
+                     return x.first < y.first;
+                   });
+  const uint32_t lo = (uint32_t)c->pend_lo, hi = (uint32_t)c->pend_hi;
+  const uint64_t base_lo = c->buckets[lo].base;
+  FlatArgs a{};
+  a.n_pieces = (int)c->pend_pieces.size();
+  for (int j = 0; j < a.n_pieces; ++j) {
+    FlatPiece fp = c->pend_pieces[j].second;
+    fp.dst_off += c->buckets[c->pend_pieces[j].first].base - base_lo;
+    a.pieces[j] = fp;
+  }
+  const uint64_t total = c->buckets[hi].base + c->buckets[hi].size - base_lo;
+  cudaStream_t fs;
+  GridPartials* fpart;
+  if (zero_status s = pick_flat_stream(c, &fs, &fpart)) return s;
+  const int grid = grid_for((total + 2047) / 2048, c->flat_ctas, c->sms);
+  const int slot = c->slot_base[lo];
+  a.per_cta = align_up((total + grid - 1) / grid, 8);
+  a.src_dtype = c->gdt;
+  a.dst_dtype = c->pdt;
+  a.epilogue = 1;
+  a.dst = c->flat_dst(lo);
+  a.sigma = c->cfg.grad_prescale;
+  a.st = c->st;
+  a.part = fpart;
+  a.slot = c->slots + slot;
+  a.cta_sum = c->cta_sum + (size_t)slot * kMaxGrid;
+  a.cta_flag = c->cta_flag + (size_t)slot * kMaxGrid;
+  a.cta_grid = c->cta_grid + slot;
+  a.clear_slots = (uint32_t)(c->slot_base[hi] - slot);   // one slot per batchable bucket
+  CK(launch_flatten(a, grid, fs, c->flat_vecs));
+  c->launches++;
+  c->pend_lo = c->pend_hi = -1;
+  c->pend_pieces.clear();
+  return ZERO_OK;
+}
+
+// LOCAL, small bucket k: join (or start) the pending run; the sources are resolved now
+zero_status defer_small(zero_ctx* c, uint32_t k, const void* const* grads) {
+  const auto& tmpl = c->flat_tmpl[k];
+  const bool adjacent = c->pend_lo >= 0 && (k + 1 == (uint32_t)c->pend_lo || k == (uint32_t)c->pend_hi + 1);
+  const uint64_t run = adjacent ? std::max(c->buckets[k].base + c->buckets[k].size,
+                                           c->buckets[c->pend_hi].base + c->buckets[c->pend_hi].size) -
+                                      std::min(c->buckets[k].base, c->buckets[c->pend_lo].base)
+                                : 0;
+  if (!adjacent || c->pend_pieces.size() + tmpl.size() > (size_t)kMaxFlatPieces || run > 4 * c->small_bucket)
+    if (zero_status s = flush_small(c)) return s;
+  const int ebytes = c->gdt == DT_F32 ? 4 : 2;
+  for (size_t j = 0; j < tmpl.size(); ++j) {
+    FlatPiece fp = tmpl[j];
+    const uint32_t t = c->flat_tensor[k][j];
+    if (t != UINT32_MAX) {
+      const char* base = reinterpret_cast<const char*>(grads[t]);
+      if (!base) return c->fail(ZERO_EINVAL, "gradient pointer of tensor %u is NULL", t);
+      fp.src = base + c->flat_toff[k][j] * ebytes;
+    }
+    c->pend_pieces.emplace_back(k, fp);
+  }
+  if (c->pend_lo < 0) c->pend_lo = c->pend_hi = (int)k;
+  c->pend_lo = std::min(c->pend_lo, (int)k);
+  c->pend_hi = std::max(c->pend_hi, (int)k);
+  return ZERO_OK;
+}
+
 // pull reduce-scatter of bucket k for rank c (PEER), sources = every member's flattened bucket
 zero_status issue_pull_rs(zero_ctx* c, ZeroGroup* g, uint32_t k) {
   const uint64_t sl = c->slice(k);
@@ -973,7 +1124,7 @@ zero_status issue_pull_rs(zero_ctx* c, ZeroGroup* g, uint32_t k) {
   a.st = c->st;
   a.part = c->part_comm;
   a.slot = c->slots + c->slot_base[k];
-  CK(launch_reduce_scatter(a, grid_for((sl + 2047) / 2048, 4, c->sms), c->comm_stream));
+  CK(launch_reduce_scatter(a, rs_setup(c, k, a, sl), c->comm_stream));
   c->launches++;
   c->counters.reduce_scatter += sl * (uint64_t)(c->n_d - 1);
   return ZERO_OK;
@@ -1015,17 +1166,16 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
     CK(cudaEventRecord(ev->r0, c->stream));
     c->step_open = true;
   }
-  // the stream this bucket is flattened on: the caller's, or one of two forked streams
-  cudaStream_t fs = c->stream;
-  GridPartials* fpart = c->part_compute;
-  if (c->n_flat_streams > 1) {
-    const int i = (int)(c->flat_rr++ % (uint32_t)c->n_flat_streams);
-    fs = c->flat_stream[i];
-    fpart = c->part_flat[i];
-    CK(cudaEventRecord(c->ev_fork, c->stream));
-    CK(cudaStreamWaitEvent(fs, c->ev_fork, 0));
-    c->flat_used[i] = true;
+  if (batchable(c, k)) {   // N_d = 1, small bucket: flattened together with its neighbours
+    if (zero_status s = defer_small(c, k, grads)) return s;
+    return finish_bucket_local(c, k);
   }
+  if (c->transport == ZERO_TRANSPORT_LOCAL)
+    if (zero_status s = flush_small(c)) return s;
+  // the stream this bucket is flattened on: the caller's, or one of the forked streams
+  cudaStream_t fs;
+  GridPartials* fpart;
+  if (zero_status s = pick_flat_stream(c, &fs, &fpart)) return s;
   if (pooled && c->transport == ZERO_TRANSPORT_NCCL) CK(cudaStreamWaitEvent(fs, c->ev_pool_free[ps], 0));
   if (pooled && c->ipc) {  // every peer finished reading this slot's previous bucket
     const auto& pl = c->pool_last[ps];
@@ -1071,7 +1221,7 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
     a.st = c->st;
     a.part = c->part_comm;
     a.slot = c->slots + c->slot_base[k];
-    CK(launch_reduce_scatter(a, grid_for((sl + 2047) / 2048, 4, c->sms), c->comm_stream));
+    CK(launch_reduce_scatter(a, rs_setup(c, k, a, sl), c->comm_stream));
     c->launches++;
     c->counters.reduce_scatter += sl * (uint64_t)(c->n_d - 1);
     if (c->stage == 0) {  // all-reduce = RS + AG of the reduced slices
@@ -1125,10 +1275,8 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
       if (++g->reduced_buckets == c->info.n_buckets) {
         for (int j = 0; j < g->n; ++j) {
           zero_ctx* cj = g->ranks[j];
-          if (launch_decide_local(cj->slots, cj->n_slots, cj->my_partial, cj->comm_stream,
-                                  cj->use_slot_w ? cj->slot_w : nullptr) != cudaSuccess)
+          if (issue_decide_local(cj, cj->comm_stream) != cudaSuccess)
             return cj->fail(ZERO_ECUDA, "decide_local launch failed");
-          cj->launches++;
         }
       }
     }
@@ -1159,7 +1307,7 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
   a.st = c->st;
   a.part = c->part_comm;
   a.slot = c->slots + c->slot_base[k];
-  CK(launch_reduce_scatter(a, grid_for((sl + 2047) / 2048, 4, c->sms), c->comm_stream));
+  CK(launch_reduce_scatter(a, rs_setup(c, k, a, sl), c->comm_stream));
   c->launches++;
   if (pooled) CK(cudaEventRecord(c->ev_pool_free[ps], c->comm_stream));
   return finish_bucket_local(c, k);
@@ -1239,7 +1387,7 @@ namespace {
 
 // zero_step, first half: join the reduce phase and form the decision inputs (the
 // per-rank {sum of squares, overflow} partials, exchanged across the data-parallel group)
-zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev) {
+zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev, bool* decided = nullptr) {
   if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
   if (zero_status ps = poll_nccl(c)) return ps;
   if (c->step_begun) return c->fail(ZERO_ESTATE, "zero_step_begin already issued: finish with zero_step_end");
@@ -1254,6 +1402,11 @@ zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev)
                    c->info.n_buckets);
   }
 
+  if (zero_status s = flush_small(c)) return s;   // the pending run of small buckets (N_d = 1)
+  if (c->gather_stream) {  // no rank's Adam may rewrite a shard a gather still reads
+    CK(cudaEventRecord(c->ev_gjoin, c->gather_stream));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_gjoin, 0));
+  }
   for (int i = 0; i < zero_ctx::kMaxFlatStreams; ++i) {  // join the flatten streams into the step
     if (!c->flat_used[i]) continue;
     CK(cudaEventRecord(c->ev_join[i], c->flat_stream[i]));
@@ -1268,19 +1421,11 @@ zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev)
   }
   pp = PartialPtrs{};
   if (c->transport == ZERO_TRANSPORT_LOCAL) {
-    const bool cp = c->flat_cta_partials;
-    if (cp && c->n_slots <= kMaxGrid)   // the flattens left per-CTA partials; part_compute is free
-      CK(launch_decide_local_slots(c->n_slots, c->my_partial, c->comm_stream, c->use_slot_w ? c->slot_w : nullptr,
-                                   c->cta_sum, c->cta_flag, c->cta_grid, c->part_compute));
-    else
-      CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream, c->use_slot_w ? c->slot_w : nullptr,
-                             cp ? c->cta_sum : nullptr, cp ? c->cta_flag : nullptr, cp ? c->cta_grid : nullptr));
-    c->launches++;
+    CK(issue_decide_local(c, c->comm_stream, decided));   // the flattens left per-CTA partials
     pp.p[0] = c->my_partial;
     pp.n = 1;
   } else if (c->ipc) {  // push my partial into every peer's gathered[rank], then wait for all
-    CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream, c->use_slot_w ? c->slot_w : nullptr));
-    c->launches++;
+    CK(issue_decide_local(c, c->comm_stream));
     PushArgs pa{};
     pa.mine = c->my_partial;
     for (int j = 0; j < c->n_d; ++j) {
@@ -1299,8 +1444,7 @@ zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev)
     for (int j = 0; j < g->n; ++j) pp.p[j] = g->ranks[j]->my_partial;
     pp.n = g->n;
   } else {
-    CK(launch_decide_local(c->slots, c->n_slots, c->my_partial, c->comm_stream, c->use_slot_w ? c->slot_w : nullptr));
-    c->launches++;
+    CK(issue_decide_local(c, c->comm_stream));
     NK(ncclAllGather(c->my_partial, c->gathered, 2, ncclFloat64, c->comm, c->comm_stream));
     for (int j = 0; j < c->n_d; ++j) pp.p[j] = c->gathered + j;
     pp.n = c->n_d;
@@ -1309,10 +1453,13 @@ zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev)
 }
 
 // zero_step, second half: decision, fused Adam + recast, all-gather, bookkeeping
-zero_status step_finish(zero_ctx* c, const PartialPtrs& pp, zero_ctx::StepEvents* ev, zero_step_info* host_out) {
+zero_status step_finish(zero_ctx* c, const PartialPtrs& pp, zero_ctx::StepEvents* ev, zero_step_info* host_out,
+                        bool decided = false) {
   ZeroGroup* g = c->group;
-  CK(launch_decide_global(pp, c->st, decide_params(c), c->comm_stream));
-  c->launches++;
+  if (!decided) {
+    CK(launch_decide_global(pp, c->st, decide_params(c), c->comm_stream));
+    c->launches++;
+  }
   if (ev) CK(cudaEventRecord(ev->a0, c->comm_stream));
   zero_status s = issue_adam(c, g);
   if (s != ZERO_OK) return s;
@@ -1343,6 +1490,7 @@ zero_status step_finish(zero_ctx* c, const PartialPtrs& pp, zero_ctx::StepEvents
     CK(launch_wait(w, c->comm_stream));
     c->launches += 2;
   }
+  if (c->ev_params) CK(cudaEventRecord(c->ev_params, c->comm_stream));   // every shard is final
   if (host_out)
     CK(cudaMemcpyAsync(host_out, &c->st->rec_t, sizeof(zero_step_info), cudaMemcpyDeviceToHost, c->comm_stream));
   if (ev) {
@@ -1390,9 +1538,10 @@ zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
   NvtxRange nvtx("zero_step");
   PartialPtrs pp{};
   zero_ctx::StepEvents* ev = nullptr;
-  zero_status s = step_inputs(c, pp, ev);
+  bool decided = false;
+  zero_status s = step_inputs(c, pp, ev, &decided);
   if (s != ZERO_OK) return s;
-  return step_finish(c, pp, ev, host_out);
+  return step_finish(c, pp, ev, host_out, decided);
 }
 
 zero_status zero_step_begin(zero_ctx* c) {
@@ -1567,6 +1716,7 @@ zero_status zero_peer_open(zero_ctx* c, const void* const* blobs, size_t blob_by
     c->own_comm_stream = true;
   }
   c->n_flat_streams = c->n_flat_streams_req;
+  if (c->stage == 3 && !c->gather_stream) CK(cudaStreamCreateWithFlags(&c->gather_stream, cudaStreamNonBlocking));
   return create_flat_streams(c);
 }
 
@@ -1614,6 +1764,11 @@ zero_status issue_layer_gather(zero_ctx* c, int li, int slot) {
     CK(cudaEventRecord(gs.ready, c->comm_stream));
   } else {  // PEER: pull every rank's shard slice
     ZeroGroup* g = c->group;
+    cudaStream_t gst = c->gather_stream ? c->gather_stream : c->stream;   // simulated ranks: the shared stream
+    if (c->gather_stream) {
+      CK(cudaStreamWaitEvent(gst, c->ev_params, 0));   // the shards of this epoch are final
+      CK(cudaStreamWaitEvent(gst, gs.freed, 0));       // the slot's previous layer is released
+    }
     for (uint32_t k = L.k0; k < L.k1; ++k) {
       const zero_bucket& b = c->buckets[k];
       const uint64_t sl = c->slice(k);
@@ -1624,10 +1779,11 @@ zero_status issue_layer_gather(zero_ctx* c, int li, int slot) {
       }
       a.count = sl;
       a.n = c->n_d;
-      CK(launch_copy(a, grid_for((sl + 2047) / 2048, 2, c->sms), c->stream));
+      CK(launch_copy(a, grid_for((sl + 2047) / 2048, 2, c->sms), gst));
       c->launches++;
       c->counters.all_gather += sl * (uint64_t)(c->n_d - 1);
     }
+    if (c->gather_stream) CK(cudaEventRecord(gs.ready, gst));
   }
   gs.layer = L.layer;
   gs.released = false;
@@ -1691,7 +1847,7 @@ zero_status zero_gather_params(zero_ctx* c, uint32_t layer, void** views_out) {
       if (r != ZERO_OK) return r;
       c->gslots[fs].released = true;  // prefetched: reusable until someone asks for it
     }
-    if (c->transport == ZERO_TRANSPORT_NCCL) CK(cudaStreamWaitEvent(c->stream, c->gslots[s].ready, 0));
+    if (c->transport == ZERO_TRANSPORT_NCCL || c->gather_stream) CK(cudaStreamWaitEvent(c->stream, c->gslots[s].ready, 0));
     base = c->gather + (uint64_t)s * c->max_layer;
   }
   if (views_out) {
@@ -1711,7 +1867,7 @@ zero_status zero_release_params(zero_ctx* c, uint32_t layer) {
   const int s = c->layer_slot[it->second];
   if (s < 0) return c->fail(ZERO_ESTATE, "layer %u is not gathered", layer);
   c->gslots[s].released = true;
-  if (c->transport == ZERO_TRANSPORT_NCCL) CK(cudaEventRecord(c->gslots[s].freed, c->stream));
+  if (c->transport == ZERO_TRANSPORT_NCCL || c->gather_stream) CK(cudaEventRecord(c->gslots[s].freed, c->stream));
   return ZERO_OK;
 }
 
@@ -1830,12 +1986,13 @@ zero_status zero_query(const zero_ctx* cc, int what, void* out, size_t n) {
 zero_status zero_wait(zero_ctx* c, uint64_t timeout_ms) {
   STICKY(c);
   if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
-  cudaStream_t ss[zero_ctx::kMaxFlatStreams + 2];
+  cudaStream_t ss[zero_ctx::kMaxFlatStreams + 3];
   int ns = 0;
   ss[ns++] = c->stream;
   if (c->comm_stream && c->comm_stream != c->stream) ss[ns++] = c->comm_stream;
   for (int i = 0; i < zero_ctx::kMaxFlatStreams; ++i)
     if (c->flat_stream[i]) ss[ns++] = c->flat_stream[i];
+  if (c->gather_stream) ss[ns++] = c->gather_stream;
   for (int i = 0; i < ns; ++i) {
     if (!c->ev_wait[i]) CK(cudaEventCreateWithFlags(&c->ev_wait[i], cudaEventDisableTiming));
     CK(cudaEventRecord(c->ev_wait[i], ss[i]));
@@ -1906,6 +2063,12 @@ void zero_destroy(zero_ctx* c) {
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   for (auto& e : c->ev_wait) if (e) cudaEventDestroy(e);
+  if (c->gather_stream) {
+    cudaStreamSynchronize(c->gather_stream);
+    cudaStreamDestroy(c->gather_stream);
+  }
+  if (c->ev_params) cudaEventDestroy(c->ev_params);
+  if (c->ev_gjoin) cudaEventDestroy(c->ev_gjoin);
   if (c->ev_flat) cudaEventDestroy(c->ev_flat);
   if (c->ev_step) cudaEventDestroy(c->ev_step);
   if (c->own_comm_stream && c->comm_stream) cudaStreamDestroy(c->comm_stream);

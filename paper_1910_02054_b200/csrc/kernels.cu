@@ -257,6 +257,8 @@ __device__ __forceinline__ void flat_publish(const FlatArgs& a, double s, uint32
       a.cta_flag[blockIdx.x] = f;
       if (blockIdx.x == 0) *a.cta_grid = gridDim.x;
     }
+    if (blockIdx.x == 0)
+      for (uint32_t i = threadIdx.x; i < a.clear_slots; i += blockDim.x) a.cta_grid[1 + i] = 0u;
   } else {
     grid_publish(s, f, a.part, a.slot);
   }
@@ -1081,7 +1083,37 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
   } else {
     rs_body<DT, kR32, kReduce, kVec, NR, U, 1>(a, inv, sumsq, flag);
   }
-  grid_publish(sumsq, flag, a.part, a.slot, a.done_sig, a.wait_flags ? a.n : 0, a.epoch);
+  if (!a.cta_sum) {
+    grid_publish(sumsq, flag, a.part, a.slot, a.done_sig, a.wait_flags ? a.n : 0, a.epoch);
+    return;
+  }
+  // per-CTA partial (combined in a fixed order by the decision kernel)
+  __shared__ bool is_last;
+  block_reduce(sumsq, flag);
+  if (threadIdx.x == 0) {
+    a.cta_sum[blockIdx.x] = sumsq;
+    a.cta_flag[blockIdx.x] = flag;
+    if (blockIdx.x == 0) *a.cta_grid = gridDim.x;
+  }
+  if (!a.wait_flags) return;
+  // cross-process: the last CTA to finish reading the peers' buckets tells them so
+  if (threadIdx.x == 0) is_last = atomicAdd(&a.part->ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (is_last && threadIdx.x == 0) {
+    a.part->ticket = 0;
+    __threadfence_system();
+    for (int j = 0; j < a.n; ++j) st_release_sys(a.done_sig[j], a.epoch);
+  }
+}
+
+template <int DT, bool R32, bool RED, int NR>
+cudaError_t launch_rs_u(const RSArgs& a, int grid, cudaStream_t s, int u) {
+  switch (u) {
+    case 1: k_reduce_scatter<DT, R32, RED, true, NR, 1><<<grid, kThreads, 0, s>>>(a); break;
+    case 4: k_reduce_scatter<DT, R32, RED, true, NR, 4><<<grid, kThreads, 0, s>>>(a); break;
+    default: k_reduce_scatter<DT, R32, RED, true, NR, 2><<<grid, kThreads, 0, s>>>(a); break;
+  }
+  return cudaGetLastError();
 }
 
 template <int DT, bool R32, bool RED, bool V>
@@ -1092,9 +1124,9 @@ cudaError_t launch_rs_n(const RSArgs& a, int grid, cudaStream_t s) {
     k_reduce_scatter<DT, R32, RED, true, 0, 2><<<grid, kThreads, 0, s>>>(a);
   } else {
     switch (a.n) {
-      case 2: k_reduce_scatter<DT, R32, RED, true, 2, 4><<<grid, kThreads, 0, s>>>(a); break;
-      case 4: k_reduce_scatter<DT, R32, RED, true, 4, 2><<<grid, kThreads, 0, s>>>(a); break;
-      case 8: k_reduce_scatter<DT, R32, RED, true, 8, 1><<<grid, kThreads, 0, s>>>(a); break;
+      case 2: return launch_rs_u<DT, R32, RED, 2>(a, grid, s, a.u ? a.u : 4);
+      case 4: return launch_rs_u<DT, R32, RED, 4>(a, grid, s, a.u ? a.u : 2);
+      case 8: return launch_rs_u<DT, R32, RED, 8>(a, grid, s, a.u ? a.u : 1);
       default: k_reduce_scatter<DT, R32, RED, true, 0, 1><<<grid, kThreads, 0, s>>>(a); break;
     }
   }
@@ -1119,6 +1151,8 @@ cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s) {
 // slots (ascending bucket, fixed tree) into one RankPartial; decide_global folds
 // the ranks' partials in ascending rank and advances the loss-scale machine.
 // ---------------------------------------------------------------------------
+__device__ void decide_apply(double sum, double flags, DevState* st, const DecideParams& p);
+
 __global__ void __launch_bounds__(1024) k_decide_local(Slot* slots, int n, RankPartial* out, const double* slot_w,
                                                            const double* cta_sum, const uint32_t* cta_flag,
                                                            const uint32_t* cta_grid) {
@@ -1161,7 +1195,8 @@ __global__ void __launch_bounds__(1024) k_decide_local(Slot* slots, int n, RankP
 // partials (block tree), then the last CTA to finish combines the slots in slot order
 __global__ void __launch_bounds__(kThreads) k_decide_local_slots(const double* slot_w, const double* cta_sum,
                                                                  const uint32_t* cta_flag, const uint32_t* cta_grid,
-                                                                 GridPartials* part, RankPartial* out) {
+                                                                 GridPartials* part, RankPartial* out,
+                                                                 DevState* st, const DecideParams p) {
   __shared__ bool is_last;
   const int i = blockIdx.x;
   const uint32_t g = cta_grid[i];
@@ -1194,13 +1229,15 @@ __global__ void __launch_bounds__(kThreads) k_decide_local_slots(const double* s
     out->sumsq = a;
     out->flag = b ? 1.0 : 0.0;
     part->ticket = 0;
+    if (st) decide_apply(a, b ? 1.0 : 0.0, st, p);   // N_d = 1: the rank's partial is the global one
   }
 }
 
 cudaError_t launch_decide_local_slots(int n_slots, RankPartial* out, cudaStream_t s, const double* slot_w,
                                       const double* cta_sum, const uint32_t* cta_flag, const uint32_t* cta_grid,
-                                      GridPartials* part) {
-  k_decide_local_slots<<<n_slots, kThreads, 0, s>>>(slot_w, cta_sum, cta_flag, cta_grid, part, out);
+                                      GridPartials* part, DevState* st, const DecideParams* p) {
+  k_decide_local_slots<<<n_slots, kThreads, 0, s>>>(slot_w, cta_sum, cta_flag, cta_grid, part, out, st,
+                                                    p ? *p : DecideParams{});
   return cudaGetLastError();
 }
 
@@ -1228,14 +1265,9 @@ cudaError_t launch_combine_partials(const PartialPtrs& pp, RankPartial* out, cud
   return cudaGetLastError();
 }
 
-__global__ void k_decide_global(const __grid_constant__ PartialPtrs pp, DevState* st, const DecideParams p) {
-  if (threadIdx.x != 0) return;
-  if (pp.wait_flags) wait_all(pp.wait_flags, pp.n, pp.epoch);
-  double sum = 0.0, flags = 0.0;
-  for (int r = 0; r < pp.n; ++r) {
-    sum += pp.p[r]->sumsq;
-    flags += pp.p[r]->flag;
-  }
+// the decision itself (reading c-4), one thread: overflow -> skip + back off the loss
+// scale; else the clip coefficient, t, the bias-correction scalars and the scale growth
+__device__ void decide_apply(double sum, double flags, DevState* st, const DecideParams& p) {
   const bool overflow = flags != 0.0;
   const float S_used = st->S;
   const double norm = sqrt(sum);
@@ -1271,6 +1303,17 @@ __global__ void k_decide_global(const __grid_constant__ PartialPtrs pp, DevState
   st->rec_clip = clip;
   st->rec_pad = 0;
   st->rec_norm = norm;
+}
+
+__global__ void k_decide_global(const __grid_constant__ PartialPtrs pp, DevState* st, const DecideParams p) {
+  if (threadIdx.x != 0) return;
+  if (pp.wait_flags) wait_all(pp.wait_flags, pp.n, pp.epoch);
+  double sum = 0.0, flags = 0.0;
+  for (int r = 0; r < pp.n; ++r) {
+    sum += pp.p[r]->sumsq;
+    flags += pp.p[r]->flag;
+  }
+  decide_apply(sum, flags, st, p);
 }
 
 cudaError_t launch_decide_global(const PartialPtrs& partials, DevState* st, DecideParams p, cudaStream_t s) {

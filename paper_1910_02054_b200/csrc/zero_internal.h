@@ -83,6 +83,8 @@ struct FlatArgs {
   double* cta_sum;
   uint32_t* cta_flag;
   uint32_t* cta_grid;
+  uint32_t clear_slots;     // batched small buckets: the next clear_slots slots' cta_grid := 0 (their
+                            // elements' partials are this launch's, in cta_grid[0]'s slot)
   int pdl;                  // host: launch as a programmatic dependent of the previous flatten
 };
 
@@ -102,6 +104,13 @@ struct RSArgs {
   const DevState* st;
   GridPartials* part;
   Slot* slot;
+  // per-CTA epilogue partials of this bucket's slot (k_decide_local combines them in a
+  // fixed order; no serial last-CTA combine at the end of every launch); NULL = grid_publish.
+  // With done_sig, part->ticket still elects the last CTA, which only signals the peers.
+  double* cta_sum;
+  uint32_t* cta_flag;
+  uint32_t* cta_grid;
+  int u;                        // host: 8-element groups per thread per iteration (0 = default)
 };
 
 struct AdamSeg {
@@ -195,10 +204,11 @@ cudaError_t launch_wait(const WaitArgs& a, cudaStream_t s);
 cudaError_t launch_handshake(const SigArgs& a, const uint64_t* my_flags, uint64_t timeout_ns, uint32_t* result,
                              cudaStream_t s);
 cudaError_t launch_push_partial(const PushArgs& a, cudaStream_t s);
-// N_d = 1 per-CTA flatten partials, one CTA per slot + a last-CTA combine (n_slots <= kMaxGrid)
+// per-CTA epilogue partials, one CTA per slot + a last-CTA combine (n_slots <= kMaxGrid); with
+// st != NULL (N_d = 1, zero_step) the last CTA also makes the decision (k_decide_global fused)
 cudaError_t launch_decide_local_slots(int n_slots, RankPartial* out, cudaStream_t s, const double* slot_w,
                                       const double* cta_sum, const uint32_t* cta_flag, const uint32_t* cta_grid,
-                                      GridPartials* part);
+                                      GridPartials* part, DevState* st = nullptr, const DecideParams* p = nullptr);
 // zero_step_begin: sum the partials of pp (waiting on its flags) into *out
 cudaError_t launch_combine_partials(const PartialPtrs& pp, RankPartial* out, cudaStream_t s);
 cudaError_t launch_decide_global(const PartialPtrs& partials, DevState* st, DecideParams p, cudaStream_t s);

@@ -284,3 +284,70 @@ def test_open_without_peer_times_out():
         msgs.append(q.get())
     assert not hung, f"workers hung: {msgs}"
     assert sorted(msgs) == ["ok", "ok"], msgs
+
+
+def _gather_overlap_worker(rank, world, port, q, distinct=False):
+    """Stage-3 layer gathers over the CUDA-IPC peer table run on the library's gather
+    stream (the parameter all-gather is pipelined across the forward/backward):
+    while the caller's compute stream is busy with a long kernel, the gather of layer 0
+    and the prefetch of layer 1 complete and can be read from a third stream."""
+    import sys
+    import time
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "tests")]
+    try:
+        import numpy as np
+        import torch.distributed as dist
+        import synth
+        from harness import bits16, zcfg_from_oracle
+        from oracle import step as OS
+        from paper_1910_02054_b200 import ZeroEngine
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(rank if distinct else 0)
+        ts = synth.mlp_layout((512, 256, 256, 128))
+        cfg = OS.AdamConfig.defaults("bf16")
+        e = ZeroEngine([t.numel for t in ts], [t.layer for t in ts], world, rank, 3, zcfg_from_oracle(cfg), "peer",
+                       align=64, bucket_cap=1 << 14)
+        e.link_peers()
+        masters = synth.master_values(ts, 1)
+        e.load_master([torch.from_numpy(a).cuda() for a in masters])
+        ost = OS.init_state(masters, cfg)
+        torch.cuda.synchronize()
+        dist.barrier()                                 # every rank's shard is loaded
+        side = torch.cuda.Stream()
+        caller = torch.cuda.current_stream()
+        torch.cuda._sleep(int(4e9))                    # ~2 s of "layer compute" on the caller's stream
+        t0 = time.time()
+        v0 = e.gather_params(0)                        # gathers layer 0, prefetches layer 1
+        time.sleep(0.3)
+        with torch.cuda.stream(side):
+            got0 = {t: bits16(v) for t, v in v0.items()}
+        busy0 = not caller.query()
+        v1 = e.gather_params(1)                        # already prefetched: no new gather
+        time.sleep(0.1)
+        with torch.cuda.stream(side):
+            got1 = {t: bits16(v) for t, v in v1.items()}
+        busy1 = not caller.query()
+        host_s = time.time() - t0
+        ok = busy0 and busy1 and host_s < 1.5
+        ok = ok and all(np.array_equal(got0[t], ost.p16[t]) for t in got0)
+        ok = ok and all(np.array_equal(got1[t], ost.p16[t]) for t in got1)
+        torch.cuda.synchronize()
+        e.release_params(0)
+        e.release_params(1)
+        dist.barrier()
+        e.destroy()
+        dist.destroy_process_group()
+        q.put("ok" if ok else f"rank {rank}: busy {busy0} {busy1} host {host_s:.2f}s, "
+              f"layer0 {[np.array_equal(got0[t], ost.p16[t]) for t in got0]}, "
+              f"layer1 {[np.array_equal(got1[t], ost.p16[t]) for t in got1]}")
+    except Exception:
+        import traceback
+        q.put(traceback.format_exc())
+        raise
+
+
+def test_stage3_gathers_overlap_compute():
+    msgs = run_workers(_gather_overlap_worker, 2)
+    assert msgs == ["ok", "ok"], msgs

@@ -210,3 +210,9 @@ def _nccl_hang_worker(rank, world, port, q):
 def test_nccl_watchdog_names_the_rank_of_a_hung_collective():
     msgs = run_workers(_nccl_hang_worker, 2, timeout=180)
     assert sorted(msgs) == ["ok", "ok"], msgs
+
+
+def test_stage3_gathers_overlap_compute_one_gpu_per_rank():
+    from test_gpu_ipc import _gather_overlap_worker
+    msgs = run_workers(_gather_overlap_worker, 2, post=(True,))
+    assert msgs == ["ok", "ok"], msgs
