@@ -3,8 +3,8 @@
 // declared in include/zero_b200.h; the partition rule is reading R-Pa1.
 //
 // The hot ops are HBM / NVLink / PCIe copies with no arithmetic:
-//   save     this rank's slice of the replicated checkpoint -> the device store (one
-//            128-bit copy kernel), or -> pinned host memory (P_a+cpu: a D2H on the
+//   save     this rank's slice of the replicated checkpoint -> the device store (the
+//            engine's 128-bit copy kernel k_copy), or -> pinned host memory (P_a+cpu: a D2H on the
 //            copy engine);
 //   prefetch P_a+cpu: the slice -> the device staging slot (H2D, copy engine);
 //   gather   every MP rank's slice -> the replicated checkpoint: PEER pulls all N_m
@@ -27,43 +27,7 @@ namespace {
 using zero::kMaxRanks;
 using zero::kThreads;
 
-// dst[j][0..count[j]) = src[j][0..count[j]) for j < n (16-bit elements, bitwise)
-struct PaCopyArgs {
-  const uint16_t* src[kMaxRanks];
-  uint16_t* dst[kMaxRanks];
-  uint64_t count[kMaxRanks];
-  int n;
-};
-
-__global__ void __launch_bounds__(kThreads) k_pa_copy(const __grid_constant__ PaCopyArgs a) {
-  const int j = blockIdx.y;
-  const uint16_t* src = a.src[j];
-  uint16_t* dst = a.dst[j];
-  const uint64_t count = a.count[j];
-  const uint64_t tid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
-  const uint64_t nthr = (uint64_t)gridDim.x * kThreads;
-  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
-    const uint64_t nv = count / 8;
-    const uint4* s4 = reinterpret_cast<const uint4*>(src);
-    uint4* d4 = reinterpret_cast<uint4*>(dst);
-    uint64_t i = tid;
-    for (; i + 3 * nthr < nv; i += 4 * nthr) {  // 4 x 128-bit loads in flight per thread
-      uint4 r0, r1, r2, r3;
-      asm volatile("ld.global.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(r0.x), "=r"(r0.y), "=r"(r0.z), "=r"(r0.w) : "l"(s4 + i));
-      asm volatile("ld.global.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(r1.x), "=r"(r1.y), "=r"(r1.z), "=r"(r1.w) : "l"(s4 + i + nthr));
-      asm volatile("ld.global.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(r2.x), "=r"(r2.y), "=r"(r2.z), "=r"(r2.w) : "l"(s4 + i + 2 * nthr));
-      asm volatile("ld.global.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(r3.x), "=r"(r3.y), "=r"(r3.z), "=r"(r3.w) : "l"(s4 + i + 3 * nthr));
-      d4[i] = r0;
-      d4[i + nthr] = r1;
-      d4[i + 2 * nthr] = r2;
-      d4[i + 3 * nthr] = r3;
-    }
-    for (; i < nv; i += nthr) d4[i] = s4[i];
-    for (uint64_t e = nv * 8 + tid; e < count; e += nthr) dst[e] = src[e];
-  } else {
-    for (uint64_t e = tid; e < count; e += nthr) dst[e] = src[e];
-  }
-}
+using PaCopyArgs = zero::CopyArgs;   // the engine's multi-row 16-bit copy kernel (k_copy)
 
 int sm_count_dev() {
   int dev = 0, n = 148;
@@ -79,9 +43,7 @@ cudaError_t launch_pa_copy(const PaCopyArgs& a, cudaStream_t s) {
   // enough CTAs per source row to fill the GPU: rows x blocks ~ 4 CTAs per SM
   const uint64_t want = (mx + (uint64_t)kThreads * 32 - 1) / ((uint64_t)kThreads * 32);
   const int per_row = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)(4 * sms + a.n - 1) / a.n));
-  dim3 g(per_row, a.n);
-  k_pa_copy<<<g, kThreads, 0, s>>>(a);
-  return cudaGetLastError();
+  return zero::launch_copy(a, per_row, s);
 }
 
 thread_local std::string g_pa_init_error;

@@ -201,6 +201,7 @@ struct zero_ctx {
   bool flat_cta_partials = true;                   // ZERO_FLAT_CTA_PARTIALS=0: last-CTA combine in each flatten
   bool rs_cta_partials = true;                     // ZERO_RS_CTA_PARTIALS=0: last-CTA combine in each reduce-scatter
   int rs_ctas = 4, rs_u = 0;                       // ZERO_RS_CTAS (CTAs per SM), ZERO_RS_U (0 = per-N default)
+  int rs_pipe = 0;                                 // ZERO_RS_PIPE: the software-pipelined pull
   // ZeRO x MP (R-MP1): per-slot norm weights (0 for MP-replicated buckets on MP rank > 0)
   double* slot_w = nullptr;
   std::vector<double> slot_w_host;
@@ -411,6 +412,7 @@ int rs_setup(const zero_ctx* c, uint32_t k, RSArgs& a, uint64_t sl) {
     a.cta_grid = c->cta_grid + slot;
   }
   a.u = c->rs_u;
+  a.pipe = c->rs_pipe;
   return grid_for((sl + 2047) / 2048, c->rs_ctas, c->sms);
 }
 
@@ -762,6 +764,7 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   if (const char* ev = getenv("ZERO_RS_CTA_PARTIALS")) c->rs_cta_partials = atoi(ev) != 0;
   if (const char* ev = getenv("ZERO_RS_CTAS")) c->rs_ctas = std::max(1, std::min(8, atoi(ev)));
   if (const char* ev = getenv("ZERO_RS_U")) c->rs_u = atoi(ev);
+  if (const char* ev = getenv("ZERO_RS_PIPE")) c->rs_pipe = atoi(ev);
   if (const char* ev = getenv("ZERO_SMALL_BUCKET")) c->small_bucket = strtoull(ev, nullptr, 10);
   if (const char* ev = getenv("ZERO_FLAT_STREAMS"))
     c->n_flat_streams = std::max(1, std::min(zero_ctx::kMaxFlatStreams, atoi(ev)));
@@ -1234,7 +1237,7 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
         ca.src[i] = c->peer_grad[i] + b.base + (uint64_t)i * sl;
         ca.dst[i] = c->grad + b.base + (uint64_t)i * sl;
       }
-      ca.count = sl;
+      for (int i = 0; i < c->n_d; ++i) ca.count[i] = sl;
       ca.n = c->n_d;
       CK(launch_copy(ca, grid_for((sl + 2047) / 2048, 2, c->sms), c->comm_stream));
       c->launches++;
@@ -1262,7 +1265,7 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
             a.src[i] = g->ranks[i]->grad + cj->buckets[k].base + (uint64_t)i * sl;
             a.dst[i] = cj->grad + cj->buckets[k].base + (uint64_t)i * sl;
           }
-          a.count = sl;
+          for (int i = 0; i < g->n; ++i) a.count[i] = sl;
           a.n = g->n;
           zero_ctx* cc = cj;
           if (launch_copy(a, grid_for((sl + 2047) / 2048, 2, cc->sms), cc->comm_stream) != cudaSuccess)
@@ -1777,7 +1780,7 @@ zero_status issue_layer_gather(zero_ctx* c, int li, int slot) {
         a.src[j] = (g ? g->ranks[j]->p16 : c->peer_p16[j]) + b.shard_off;
         a.dst[j] = dst + (b.base - L.flat0) + (uint64_t)j * sl;
       }
-      a.count = sl;
+      for (int j = 0; j < c->n_d; ++j) a.count[j] = sl;
       a.n = c->n_d;
       CK(launch_copy(a, grid_for((sl + 2047) / 2048, 2, c->sms), gst));
       c->launches++;

@@ -1067,6 +1067,53 @@ __device__ __forceinline__ void rs_body(const RSArgs& a, float inv, double& sums
   }
 }
 
+// software-pipelined pull (NR ranks, 16-B groups): the NR loads of a thread's next group are
+// issued before the current group is summed and stored, so every thread keeps two groups of
+// loads in flight and a partial last round costs only its own bytes
+template <int DT, bool kR32, int NR, int kEpi>
+__device__ __forceinline__ void rs_body_pipe(const RSArgs& a, float inv, double& sumsq, uint32_t& flag) {
+  using D = H16<DT>;
+  const uint64_t nvec = a.count / 8;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  const uint64_t first = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  U4 cur[NR], nxt[NR];
+  if (first < nvec) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) cur[r] = ld128(reinterpret_cast<const uint16_t*>(a.src[r]) + first * 8);
+  }
+#pragma unroll 1
+  for (uint64_t g = first; g < nvec; g += stride) {
+    const uint64_t gn = g + stride;
+    if (gn < nvec) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r) nxt[r] = ld128(reinterpret_cast<const uint16_t*>(a.src[r]) + gn * 8);
+    }
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = D::widen(h_get(cur[0], j));
+#pragma unroll
+    for (int r = 1; r < NR; ++r) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], D::widen(h_get(cur[r], j)));
+    }
+    rs_emit8<DT, kR32, kEpi>(a, g * 8, acc, true, inv, sumsq, flag);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) cur[r] = nxt[r];
+  }
+  for (uint64_t k = nvec * 8 + first; k < a.count; k += stride) {   // ragged tail (< 8 elements)
+    float acc = D::widen(reinterpret_cast<const uint16_t*>(a.src[0])[k]);
+    for (int r = 1; r < NR; ++r) acc = __fadd_rn(acc, D::widen(reinterpret_cast<const uint16_t*>(a.src[r])[k]));
+    if (kR32) {
+      reinterpret_cast<float*>(a.dst)[k] = acc;
+      rs_epi<DT, true, kEpi>(acc, 0u, inv, sumsq, flag);
+    } else {
+      const uint32_t b = D::narrow(acc);
+      reinterpret_cast<uint16_t*>(a.dst)[k] = (uint16_t)b;
+      rs_epi<DT, false, kEpi>(0.0f, b, inv, sumsq, flag);
+    }
+  }
+}
+
 template <int DT, bool kR32, bool kReduce, bool kVec, int NR, int U>
 __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_constant__ RSArgs a) {
   if (a.wait_flags) {  // every rank has flattened this bucket (cross-process PEER)
@@ -1076,12 +1123,15 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
   const float inv = a.st->inv_cur;
   double sumsq = 0.0;
   uint32_t flag = 0;
+  constexpr bool kPipe = U == 0;   // U = 0 selects the software-pipelined pull
   if (pow2_at_most_one(inv)) {   // inv = 1/(N S sigma) a power of two (N a power of two)
-    rs_body<DT, kR32, kReduce, kVec, NR, U, 2>(a, inv, sumsq, flag);
+    if constexpr (kPipe) rs_body_pipe<DT, kR32, NR, 2>(a, inv, sumsq, flag);
+    else rs_body<DT, kR32, kReduce, kVec, NR, U, 2>(a, inv, sumsq, flag);
     flag = isfinite(sumsq) ? 0u : 1u;     // G^2 / b^2 of finite values are finite in fp64
     sumsq *= (double)inv * (double)inv;   // exact
   } else {
-    rs_body<DT, kR32, kReduce, kVec, NR, U, 1>(a, inv, sumsq, flag);
+    if constexpr (kPipe) rs_body_pipe<DT, kR32, NR, 1>(a, inv, sumsq, flag);
+    else rs_body<DT, kR32, kReduce, kVec, NR, U, 1>(a, inv, sumsq, flag);
   }
   if (!a.cta_sum) {
     grid_publish(sumsq, flag, a.part, a.slot, a.done_sig, a.wait_flags ? a.n : 0, a.epoch);
@@ -1108,6 +1158,10 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
 
 template <int DT, bool R32, bool RED, int NR>
 cudaError_t launch_rs_u(const RSArgs& a, int grid, cudaStream_t s, int u) {
+  if (a.pipe) {
+    k_reduce_scatter<DT, R32, RED, true, NR, 0><<<grid, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+  }
   switch (u) {
     case 1: k_reduce_scatter<DT, R32, RED, true, NR, 1><<<grid, kThreads, 0, s>>>(a); break;
     case 4: k_reduce_scatter<DT, R32, RED, true, NR, 4><<<grid, kThreads, 0, s>>>(a); break;
@@ -1841,17 +1895,19 @@ cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int variant
 }
 
 // ---------------------------------------------------------------------------
-// a6/a7 over a peer table: dst[j][0..count) = src[j][0..count) (16-bit, bitwise)
+// a6/a7 over a peer table (and P_a's save / gather): dst[j][0..count[j]) = src[j][0..count[j])
+// for every row j < n (16-bit, bitwise)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ CopyArgs a) {
   const int j = blockIdx.y;
   const uint16_t* src = reinterpret_cast<const uint16_t*>(a.src[j]);
   uint16_t* dst = reinterpret_cast<uint16_t*>(a.dst[j]);
+  const uint64_t count = a.count[j];
   if (src == dst) return;
   const uint64_t tid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
   const uint64_t nthr = (uint64_t)gridDim.x * kThreads;
   if (aligned(src, 16) && aligned(dst, 16)) {
-    const uint64_t nv = a.count / 8;
+    const uint64_t nv = count / 8;
     uint64_t i = tid;
     for (; i + 3 * nthr < nv; i += 4 * nthr) {   // 4 x 128-bit loads in flight (NVLink latency ~2 us)
       const U4 r0 = ld128(src + i * 8), r1 = ld128(src + (i + nthr) * 8);
@@ -1862,14 +1918,16 @@ __global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ CopyA
       st128(dst + (i + 3 * nthr) * 8, r3);
     }
     for (; i < nv; i += nthr) st128(dst + i * 8, ld128(src + i * 8));
-    for (uint64_t e = nv * 8 + tid; e < a.count; e += nthr) dst[e] = src[e];
+    for (uint64_t e = nv * 8 + tid; e < count; e += nthr) dst[e] = src[e];
   } else {
-    for (uint64_t i = tid; i < a.count; i += nthr) dst[i] = src[i];
+    for (uint64_t i = tid; i < count; i += nthr) dst[i] = src[i];
   }
 }
 
 cudaError_t launch_copy(const CopyArgs& a, int grid, cudaStream_t s) {
-  if (a.n <= 0 || a.count == 0) return cudaSuccess;
+  uint64_t mx = 0;
+  for (int j = 0; j < a.n; ++j) mx = a.count[j] > mx ? a.count[j] : mx;
+  if (a.n <= 0 || mx == 0) return cudaSuccess;
   dim3 g(grid, a.n);
   k_copy<<<g, kThreads, 0, s>>>(a);
   return cudaGetLastError();

@@ -111,6 +111,7 @@ struct RSArgs {
   uint32_t* cta_flag;
   uint32_t* cta_grid;
   int u;                        // host: 8-element groups per thread per iteration (0 = default)
+  int pipe;                     // host: software-pipelined variant (next group's loads in flight)
 };
 
 struct AdamSeg {
@@ -134,10 +135,10 @@ struct AdamArgs {
   const DevState* st;
 };
 
-struct CopyArgs {             // multi-source 16-bit copy (pull all-gather)
+struct CopyArgs {             // multi-row 16-bit copy: pull all-gathers (a6/a7) and P_a's save/gather
   const void* src[kMaxRanks];
   void* dst[kMaxRanks];
-  uint64_t count;             // elements per source
+  uint64_t count[kMaxRanks];  // elements of row j (grid row j copies src[j] -> dst[j])
   int n;
 };
 

@@ -13,11 +13,10 @@ run() {  # name, env...
 }
 run base ZERO_RS_CTA_PARTIALS=0 ZERO_RS_CTAS=4 ZERO_RS_U=2
 run p_c4_u2 ZERO_RS_CTA_PARTIALS=1 ZERO_RS_CTAS=4 ZERO_RS_U=2
-run p_c5_u2 ZERO_RS_CTA_PARTIALS=1 ZERO_RS_CTAS=5 ZERO_RS_U=2
-run p_c4_u1 ZERO_RS_CTA_PARTIALS=1 ZERO_RS_CTAS=4 ZERO_RS_U=1
 run p_c6_u1 ZERO_RS_CTA_PARTIALS=1 ZERO_RS_CTAS=6 ZERO_RS_U=1
-run p_c8_u1 ZERO_RS_CTA_PARTIALS=1 ZERO_RS_CTAS=8 ZERO_RS_U=1
-run p_c2_u4 ZERO_RS_CTA_PARTIALS=1 ZERO_RS_CTAS=2 ZERO_RS_U=4
-run p_c3_u4 ZERO_RS_CTA_PARTIALS=1 ZERO_RS_CTAS=3 ZERO_RS_U=4
+run pipe_c4 ZERO_RS_CTA_PARTIALS=1 ZERO_RS_CTAS=4 ZERO_RS_PIPE=1
+run pipe_c3 ZERO_RS_CTA_PARTIALS=1 ZERO_RS_CTAS=3 ZERO_RS_PIPE=1
+run pipe_c2 ZERO_RS_CTA_PARTIALS=1 ZERO_RS_CTAS=2 ZERO_RS_PIPE=1
+run pipe_c1 ZERO_RS_CTA_PARTIALS=1 ZERO_RS_CTAS=1 ZERO_RS_PIPE=1
 # the whole simulated step (no profiler), default variant
 timeout 600 python scripts/sim_bench.py --ranks 4 --stage 2 > gpurun_out/rs_sweep/sim_step.jsonl 2>&1

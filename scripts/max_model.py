@@ -3,17 +3,31 @@
 For GPT-style layouts of hidden size 8192 (the 60B/100B family) with L
 blocks, find the largest L whose ZeRO arenas -- exactly what zero_buffer_sizes
 asks the caller to allocate: model states, the C_B staging pool, the stage-3
-layer-gather pool and scratch -- fit one B200 (180 GB, P:38's "memory multiplier"
-accounting plus the constant-size buffers of §6.2), per stage and DP degree.
-Pure host computation through the C ABI (no GPU).  Activations and the model's
-own gradient tensors are not counted (the paper's Table 2 counts model states).
+layer-gather pool and scratch -- fit one B200, per stage and DP degree (P:38's
+"memory multiplier" accounting plus the constant-size buffers of §6.2).
+Activations and the model's own gradient tensors are not counted (the paper's
+Table 2 counts model states).
 
-  python scripts/max_model.py [--mem-gb 180] [--hidden 8192]
+  python scripts/max_model.py [--mem-gb 180] [--hidden 8192]      # host arithmetic through the C ABI
+  python scripts/max_model.py --device [--reserve-gb 4]           # validated on the GPU
+
+--device (rank 0's context of every (N_d, stage) cell, on this GPU): the budget is
+the device's free memory minus a reserve for the loader's temporary fp32 tensor;
+for the predicted L_max it runs zero_init, zero_buffer_sizes, allocates and binds
+the arenas (zeroed on the device) and loads the fp32 masters tensor by tensor
+(zero_load_master with NULL for the others: bounded temporary memory), then reads
+back zero_query(MEMORY) and checks a sample of the shard against the generator;
+with L_max + 1 blocks the arena allocation must fail with an out-of-memory error
+and leave the device usable.  Config 4 (60B = 75 x 8192, stage 3, N_d = 8) is
+instantiated the same way.  N_d > 1 cells build an unlinked PEER context: its
+arenas are exactly a real rank's (no step runs without its peers).
 """
 import argparse
+import gc
 import json
 import os
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -48,11 +62,103 @@ def max_layers(h, n, stage, mem):
     return lo
 
 
+def instantiate(L, h, n, stage, load=True):
+    """Rank 0's context of the L-block model on this GPU: arenas bound and (optionally)
+    the fp32 masters loaded one tensor at a time.  Returns a result dict."""
+    import numpy as np
+    import torch
+    from paper_1910_02054_b200 import ZeroConfig
+    ts = synth.gpt_layout(L, h, 50257, 1024)
+    dev = torch.device("cuda", 0)
+    t0 = time.time()
+    e = ZeroEngine([t.numel for t in ts], [t.layer for t in ts], n, 0, stage, ZeroConfig.defaults("bf16"),
+                   transport="local" if n == 1 else "peer", bucket_cap=1 << 26, device=dev)
+    torch.cuda.synchronize()
+    out = {"arena_bytes": sum(a.numel() for a in e.arenas.values() if a is not None)}
+    if load:
+        chunk, cur = [], 0            # <= ~1 GB of fp32 masters per call (one tensor may be larger)
+        for i, t in enumerate(ts):
+            chunk.append(i)
+            cur += t.numel
+            if cur >= (1 << 28) or i == len(ts) - 1:
+                m = synth.gpu_masters(ts, 1, dev, only=set(chunk))
+                e.load_master(m)
+                torch.cuda.synchronize()
+                del m
+                chunk, cur = [], 0
+        # spot check: the first element this rank owns of the first bucket = the generator's value
+        p32 = e.shard()[0]
+        b0 = e.buckets[0]
+        ref = synth.master_values([synth.TensorSpec("x", 16, 0)], 1)[0]      # wte's first 16 values
+        got = p32[:16].cpu().numpy()
+        out["shard_spot_check"] = bool(np.array_equal(got, ref)) if b0.base == 0 else None
+    mem = e.memory()
+    out.update({"params16": mem.params16, "grads16": mem.grads16, "optimizer": mem.optimizer,
+                "model_state_bytes": mem.params16 + mem.grads16 + mem.optimizer,
+                "staging": mem.staging, "gather_pool": mem.gather_pool, "scratch": mem.scratch,
+                "seconds": round(time.time() - t0, 1)})
+    e.destroy()
+    del e
+    gc.collect()
+    torch.cuda.empty_cache()
+    return out, synth.psi(ts)
+
+
+def over_the_top(L, h, n, stage):
+    """L blocks must not fit: the arena allocation fails with an OOM and the device stays usable."""
+    import torch
+    try:
+        instantiate(L, h, n, stage, load=False)
+        res = "fit (unexpected)"
+    except torch.OutOfMemoryError:
+        res = "out of memory"
+    gc.collect()
+    torch.cuda.empty_cache()
+    x = torch.ones(1 << 20, device="cuda")          # the device is still usable
+    ok = float(x.sum().item()) == float(1 << 20)
+    del x
+    return res, ok
+
+
+def device_main(args):
+    import torch
+    torch.cuda.init()
+    free, total = torch.cuda.mem_get_info()
+    budget = free - int(args.reserve_gb * 1e9)
+    print(json.dumps({"device": torch.cuda.get_device_name(0), "free_bytes": free, "total_bytes": total,
+                      "budget_bytes": budget, "reserve_gb": args.reserve_gb}), flush=True)
+    cells = [(1, s) for s in (0, 1, 2, 3)] + [(n, s) for n in (2, 4, 8) for s in (1, 2, 3)]
+    for n, stage in cells:
+        L = max_layers(args.hidden, n, stage, budget)
+        pred, psi = arena_bytes(L, args.hidden, n, stage)
+        row = {"n_d": n, "stage": stage, "layers": L, "psi": psi, "psi_B": round(psi / 1e9, 2),
+               "predicted_arena_bytes": pred}
+        try:
+            res, _ = instantiate(L, args.hidden, n, stage)
+            row.update(res)
+            row["fits"] = True
+        except torch.OutOfMemoryError as exc:
+            row["fits"] = False
+            row["error"] = str(exc)[:200]
+            gc.collect()
+            torch.cuda.empty_cache()
+        row["one_layer_more"], row["device_usable_after"] = over_the_top(L + 1, args.hidden, n, stage)
+        print(json.dumps(row), flush=True)
+    # config 4: 60B (75 x 8192), stage 3, N_d = 8 -- rank 0's arenas on one B200
+    res, psi = instantiate(75, 8192, 8, 3)
+    res.update({"config": "4: 60B layout (75 x 8192), ZeRO stage 3, N_d = 8, rank 0", "psi": psi, "fits": True})
+    print(json.dumps(res), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mem-gb", type=float, default=180.0)
     ap.add_argument("--hidden", type=int, default=8192)
+    ap.add_argument("--device", action="store_true")
+    ap.add_argument("--reserve-gb", type=float, default=4.0)
     args = ap.parse_args()
+    if args.device:
+        return device_main(args)
     mem = int(args.mem_gb * 1e9)
     rows = []
     for n in (1, 2, 4, 8):
