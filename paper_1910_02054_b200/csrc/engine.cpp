@@ -230,6 +230,9 @@ struct zero_ctx {
   bool segs_aligned8 = true;                       // every segment offset/count % 8 == 0
   int sms = 148;
   int adam_variant = 21;                           // ZERO_ADAM_VARIANT (tuning; 21 = TMA in/out, 4096 x 2 stages)
+  bool adam_variant_env = false;
+  uint64_t adam_small = 1ull << 21;                // ZERO_ADAM_SMALL: shards up to this size use the
+                                                   // register-staged 4-CTA/SM kernel (latency-bound sizes)
   int flat_vecs = 4, flat_ctas = 4;                // ZERO_FLAT_VECS / ZERO_FLAT_CTAS
   int flat_tma = 0;                                // ZERO_FLAT_TMA: 0 off, else the TMA variant
 
@@ -288,6 +291,8 @@ struct zero_ctx {
 
   zero_status sticky = ZERO_OK;
   std::string err;
+  const void* rec_host = nullptr;                  // the last zero_step host_out and its device alias
+  void* rec_dev = nullptr;
   bool comm_aborted = false;                       // the NCCL watchdog aborted the communicator
   cudaEvent_t ev_wait[kMaxFlatStreams + 3] = {};   // zero_wait: one per stream the context uses
 
@@ -418,14 +423,30 @@ int rs_setup(const zero_ctx* c, uint32_t k, RSArgs& a, uint64_t sl) {
 
 DecideParams decide_params(const zero_ctx* c);
 
+// the device-visible alias of the caller's pinned step record (UVA-mapped pinned memory), or
+// NULL (pageable memory: the record is copied D2H at the end of the step instead)
+void* mapped_record(zero_ctx* c, const void* host_out) {
+  if (!host_out) return nullptr;
+  if (host_out != c->rec_host) {
+    cudaPointerAttributes at{};
+    c->rec_dev = nullptr;
+    if (cudaPointerGetAttributes(&at, host_out) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
+      c->rec_dev = at.devicePointer;
+    cudaGetLastError();   // a pageable pointer is not an error
+    c->rec_host = host_out;
+  }
+  return c->rec_dev;
+}
+
 // the rank's {sum of squares, overflow} partial from the per-bucket epilogue results;
 // *decided (N_d = 1, zero_step): the same launch also made the step's decision
-cudaError_t issue_decide_local(zero_ctx* c, cudaStream_t s, bool* decided = nullptr) {
+cudaError_t issue_decide_local(zero_ctx* c, cudaStream_t s, bool* decided = nullptr, void* rec_dev = nullptr) {
   const bool cp = c->transport == ZERO_TRANSPORT_LOCAL ? c->flat_cta_partials : c->rs_cta_partials;
   const double* w = c->use_slot_w ? c->slot_w : nullptr;
   c->launches++;
   if (cp && c->n_slots <= kMaxGrid) {   // one CTA per slot, last CTA combines (part_compute is free here)
     DecideParams p = decide_params(c);
+    p.rec_out = rec_dev;
     if (decided) *decided = true;
     return launch_decide_local_slots(c->n_slots, c->my_partial, s, w, c->cta_sum, c->cta_flag, c->cta_grid,
                                      c->part_compute, decided ? c->st : nullptr, decided ? &p : nullptr);
@@ -742,7 +763,8 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   c->off_gathered = sl.gathered;
   c->pool_last.assign(c->pool, std::make_pair(-1, (uint64_t)0));
   c->sms = sm_count();
-  if (const char* ev = getenv("ZERO_ADAM_VARIANT")) c->adam_variant = atoi(ev);
+  if (const char* ev = getenv("ZERO_ADAM_VARIANT")) { c->adam_variant = atoi(ev); c->adam_variant_env = true; }
+  if (const char* ev = getenv("ZERO_ADAM_SMALL")) c->adam_small = strtoull(ev, nullptr, 10);
   if (const char* ev = getenv("ZERO_FLAT_VECS")) c->flat_vecs = atoi(ev);
   if (const char* ev = getenv("ZERO_FLAT_CTAS")) c->flat_ctas = atoi(ev);
   if (const char* ev = getenv("ZERO_FLAT_TMA")) c->flat_tma = atoi(ev);
@@ -1045,7 +1067,7 @@ bool batchable(const zero_ctx* c, uint32_t k) {
 // one launch for the pending run of adjacent small buckets [pend_lo, pend_hi] (N_d = 1): their
 // pieces tile [base_lo, base_hi + B_hi) contiguously; the epilogue partials go to the first
 // bucket's slot and the run's other slots are cleared
-zero_status flush_small(zero_ctx* c) {
+zero_status flush_small(zero_ctx* c, bool on_caller_stream = false) {
   if (c->pend_lo < 0) return ZERO_OK;
   std::stable_sort(c->pend_pieces.begin(), c->pend_pieces.end(),
                    [](const std::pair<uint32_t, FlatPiece>& x, const std::pair<uint32_t, FlatPiece>& y) {
@@ -1061,9 +1083,10 @@ zero_status flush_small(zero_ctx* c) {
     a.pieces[j] = fp;
   }
   const uint64_t total = c->buckets[hi].base + c->buckets[hi].size - base_lo;
-  cudaStream_t fs;
-  GridPartials* fpart;
-  if (zero_status s = pick_flat_stream(c, &fs, &fpart)) return s;
+  cudaStream_t fs = c->stream;
+  GridPartials* fpart = c->part_compute;
+  if (!on_caller_stream)
+    if (zero_status s = pick_flat_stream(c, &fs, &fpart)) return s;
   const int grid = grid_for((total + 2047) / 2048, c->flat_ctas, c->sms);
   const int slot = c->slot_base[lo];
   a.per_cta = align_up((total + grid - 1) / grid, 8);
@@ -1343,6 +1366,9 @@ zero_status issue_adam(zero_ctx* c, ZeroGroup* g) {
   a.n_segs = (int)c->segs_host.size();
   a.total = c->S_e;
   int variant = c->adam_variant;
+  // a small shard is a few tiles per SM: the TMA ring's fill latency dominates, so the
+  // register-staged kernel with 4 CTAs per SM is used (unless a variant is forced)
+  if (!c->adam_variant_env && c->S_e <= c->adam_small) variant = 1;
   if (adam_variant_is_tma(variant) && !c->segs_aligned8) variant = 0;  // bulk copies need 16-B granules
   const int grid = grid_for((c->S_e + 2047) / 2048, adam_ctas_per_sm(variant), c->sms);
   a.per_cta = align_up((c->S_e + grid - 1) / grid, 8);
@@ -1390,7 +1416,8 @@ namespace {
 
 // zero_step, first half: join the reduce phase and form the decision inputs (the
 // per-rank {sum of squares, overflow} partials, exchanged across the data-parallel group)
-zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev, bool* decided = nullptr) {
+zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev, bool* decided = nullptr,
+                        void* rec_dev = nullptr) {
   if (!c->bound) return c->fail(ZERO_ESTATE, "buffers not bound");
   if (zero_status ps = poll_nccl(c)) return ps;
   if (c->step_begun) return c->fail(ZERO_ESTATE, "zero_step_begin already issued: finish with zero_step_end");
@@ -1405,7 +1432,8 @@ zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev,
                    c->info.n_buckets);
   }
 
-  if (zero_status s = flush_small(c)) return s;   // the pending run of small buckets (N_d = 1)
+  // the pending run of small buckets (N_d = 1), on the caller's stream: the step follows it there
+  if (zero_status s = flush_small(c, true)) return s;
   if (c->gather_stream) {  // no rank's Adam may rewrite a shard a gather still reads
     CK(cudaEventRecord(c->ev_gjoin, c->gather_stream));
     CK(cudaStreamWaitEvent(c->comm_stream, c->ev_gjoin, 0));
@@ -1424,7 +1452,7 @@ zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev,
   }
   pp = PartialPtrs{};
   if (c->transport == ZERO_TRANSPORT_LOCAL) {
-    CK(issue_decide_local(c, c->comm_stream, decided));   // the flattens left per-CTA partials
+    CK(issue_decide_local(c, c->comm_stream, decided, rec_dev));   // the flattens left per-CTA partials
     pp.p[0] = c->my_partial;
     pp.n = 1;
   } else if (c->ipc) {  // push my partial into every peer's gathered[rank], then wait for all
@@ -1459,8 +1487,11 @@ zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev,
 zero_status step_finish(zero_ctx* c, const PartialPtrs& pp, zero_ctx::StepEvents* ev, zero_step_info* host_out,
                         bool decided = false) {
   ZeroGroup* g = c->group;
+  void* rec_dev = mapped_record(c, host_out);
   if (!decided) {
-    CK(launch_decide_global(pp, c->st, decide_params(c), c->comm_stream));
+    DecideParams p = decide_params(c);
+    p.rec_out = rec_dev;
+    CK(launch_decide_global(pp, c->st, p, c->comm_stream));
     c->launches++;
   }
   if (ev) CK(cudaEventRecord(ev->a0, c->comm_stream));
@@ -1482,7 +1513,7 @@ zero_status step_finish(zero_ctx* c, const PartialPtrs& pp, zero_ctx::StepEvents
   } else if (c->transport == ZERO_TRANSPORT_PEER && (c->stage == 1 || c->stage == 2)) {
     for (uint32_t k = 0; k < c->info.n_buckets; ++k) c->counters.all_gather += c->slice(k) * (uint64_t)(c->n_d - 1);
   }
-  if (ev) CK(cudaEventRecord(ev->g1, c->comm_stream));   // end of the separate all-gather (NCCL)
+  if (ev && c->transport == ZERO_TRANSPORT_NCCL) CK(cudaEventRecord(ev->g1, c->comm_stream));   // end of the separate AG
   if (c->ipc) {  // the replicas (stages 1/2) / shards (stage 3) are final on every rank
     SigArgs sa{};
     for (int j = 0; j < c->n_d; ++j) sa.dst[j] = c->sig(j, c->off_sig_adam, c->rank);
@@ -1494,7 +1525,7 @@ zero_status step_finish(zero_ctx* c, const PartialPtrs& pp, zero_ctx::StepEvents
     c->launches += 2;
   }
   if (c->ev_params) CK(cudaEventRecord(c->ev_params, c->comm_stream));   // every shard is final
-  if (host_out)
+  if (host_out && !rec_dev)   // pageable: copy; pinned: the decision kernel already wrote it
     CK(cudaMemcpyAsync(host_out, &c->st->rec_t, sizeof(zero_step_info), cudaMemcpyDeviceToHost, c->comm_stream));
   if (ev) {
     CK(cudaEventRecord(ev->s1, c->comm_stream));
@@ -1542,7 +1573,7 @@ zero_status zero_step(zero_ctx* c, zero_step_info* host_out) {
   PartialPtrs pp{};
   zero_ctx::StepEvents* ev = nullptr;
   bool decided = false;
-  zero_status s = step_inputs(c, pp, ev, &decided);
+  zero_status s = step_inputs(c, pp, ev, &decided, mapped_record(c, host_out));
   if (s != ZERO_OK) return s;
   return step_finish(c, pp, ev, host_out, decided);
 }
@@ -1960,7 +1991,7 @@ zero_status zero_query(const zero_ctx* cc, int what, void* out, size_t n) {
           float a = 0, b = 0, d = 0, g = 0;
           CK(cudaEventElapsedTime(&a, c->ev_pool[i].r0, c->ev_pool[i].r1));
           CK(cudaEventElapsedTime(&b, c->ev_pool[i].a0, c->ev_pool[i].a1));
-          CK(cudaEventElapsedTime(&g, c->ev_pool[i].a1, c->ev_pool[i].g1));
+          if (c->transport == ZERO_TRANSPORT_NCCL) CK(cudaEventElapsedTime(&g, c->ev_pool[i].a1, c->ev_pool[i].g1));
           CK(cudaEventElapsedTime(&d, c->ev_pool[i].r1, c->ev_pool[i].s1));
           tm.reduce_ms += a;
           tm.adam_ms += b;

@@ -1067,40 +1067,91 @@ __device__ __forceinline__ void rs_body(const RSArgs& a, float inv, double& sums
   }
 }
 
-// software-pipelined pull (NR ranks, 16-B groups): the NR loads of a thread's next group are
-// issued before the current group is summed and stored, so every thread keeps two groups of
-// loads in flight and a partial last round costs only its own bytes
-template <int DT, bool kR32, int NR, int kEpi>
-__device__ __forceinline__ void rs_body_pipe(const RSArgs& a, float inv, double& sumsq, uint32_t& flag) {
+// groups of W 16-bit elements per rank per thread (W = 8: 128-bit loads, W = 16: 256-bit);
+// PIPE: the NR loads of a thread's next group are issued before the current group is summed
+// and stored, so every thread keeps two groups in flight and a partial last round costs
+// only its own bytes
+template <int W>
+struct RSVec;
+template <>
+struct RSVec<8> {
+  using T = U4;
+  static __device__ __forceinline__ T ld(const uint16_t* p) { return ld128(p); }
+  static __device__ __forceinline__ uint32_t get(const T& v, int j) { return h_get(v, j); }
+};
+template <>
+struct RSVec<16> {
+  using T = U8;
+  static __device__ __forceinline__ T ld(const uint16_t* p) { return ld256(p); }
+  static __device__ __forceinline__ uint32_t get(const T& v, int j) { return (v.x[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu; }
+};
+
+template <int DT, bool kR32, int kEpi, int W>
+__device__ __forceinline__ void rs_emit_w(const RSArgs& a, uint64_t i, const float (&acc)[W], float inv, double& sumsq,
+                                          uint32_t& flag) {
+  if constexpr (W == 8) {
+    rs_emit8<DT, kR32, kEpi>(a, i, acc, true, inv, sumsq, flag);
+  } else {
+    float lo[8], hi[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { lo[j] = acc[j]; hi[j] = acc[8 + j]; }
+    if (kR32) {
+      rs_emit8<DT, kR32, kEpi>(a, i, lo, true, inv, sumsq, flag);
+      rs_emit8<DT, kR32, kEpi>(a, i + 8, hi, true, inv, sumsq, flag);
+    } else {   // one 256-bit store of 16 rounded values
+      using D = H16<DT>;
+      U8 o;
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        const uint32_t b0 = D::narrow(acc[j]), b1 = D::narrow(acc[j + 1]);
+        o.x[j >> 1] = b0 | (b1 << 16);
+        rs_epi<DT, false, kEpi>(0.0f, b0, inv, sumsq, flag);
+        rs_epi<DT, false, kEpi>(0.0f, b1, inv, sumsq, flag);
+      }
+      st256(reinterpret_cast<uint16_t*>(a.dst) + i, o);
+    }
+  }
+}
+
+template <int DT, bool kR32, int NR, int kEpi, int W, bool PIPE>
+__device__ __forceinline__ void rs_body_g(const RSArgs& a, float inv, double& sumsq, uint32_t& flag) {
   using D = H16<DT>;
-  const uint64_t nvec = a.count / 8;
+  using V = RSVec<W>;
+  const uint64_t nvec = a.count / W;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   const uint64_t first = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
-  U4 cur[NR], nxt[NR];
-  if (first < nvec) {
+  typename V::T cur[NR], nxt[NR];
+  if (PIPE && first < nvec) {
 #pragma unroll
-    for (int r = 0; r < NR; ++r) cur[r] = ld128(reinterpret_cast<const uint16_t*>(a.src[r]) + first * 8);
+    for (int r = 0; r < NR; ++r) cur[r] = V::ld(reinterpret_cast<const uint16_t*>(a.src[r]) + first * W);
   }
 #pragma unroll 1
   for (uint64_t g = first; g < nvec; g += stride) {
-    const uint64_t gn = g + stride;
-    if (gn < nvec) {
+    if (PIPE) {
+      const uint64_t gn = g + stride;
+      if (gn < nvec) {
 #pragma unroll
-      for (int r = 0; r < NR; ++r) nxt[r] = ld128(reinterpret_cast<const uint16_t*>(a.src[r]) + gn * 8);
+        for (int r = 0; r < NR; ++r) nxt[r] = V::ld(reinterpret_cast<const uint16_t*>(a.src[r]) + gn * W);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < NR; ++r) cur[r] = V::ld(reinterpret_cast<const uint16_t*>(a.src[r]) + g * W);
     }
-    float acc[8];
+    float acc[W];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = D::widen(h_get(cur[0], j));
+    for (int j = 0; j < W; ++j) acc[j] = D::widen(V::get(cur[0], j));
 #pragma unroll
     for (int r = 1; r < NR; ++r) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], D::widen(h_get(cur[r], j)));
+      for (int j = 0; j < W; ++j) acc[j] = __fadd_rn(acc[j], D::widen(V::get(cur[r], j)));
     }
-    rs_emit8<DT, kR32, kEpi>(a, g * 8, acc, true, inv, sumsq, flag);
+    rs_emit_w<DT, kR32, kEpi, W>(a, g * W, acc, inv, sumsq, flag);
+    if (PIPE) {
 #pragma unroll
-    for (int r = 0; r < NR; ++r) cur[r] = nxt[r];
+      for (int r = 0; r < NR; ++r) cur[r] = nxt[r];
+    }
   }
-  for (uint64_t k = nvec * 8 + first; k < a.count; k += stride) {   // ragged tail (< 8 elements)
+  for (uint64_t k = nvec * W + first; k < a.count; k += stride) {   // ragged tail (< W elements)
     float acc = D::widen(reinterpret_cast<const uint16_t*>(a.src[0])[k]);
     for (int r = 1; r < NR; ++r) acc = __fadd_rn(acc, D::widen(reinterpret_cast<const uint16_t*>(a.src[r])[k]));
     if (kR32) {
@@ -1123,14 +1174,18 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
   const float inv = a.st->inv_cur;
   double sumsq = 0.0;
   uint32_t flag = 0;
-  constexpr bool kPipe = U == 0;   // U = 0 selects the software-pipelined pull
+  // U selects the body: 1/2/4 = groups of 8 per thread per iteration; 0 = pipelined 128-bit;
+  // 16 = 256-bit loads; 17 = pipelined 256-bit
+  constexpr bool kG = U == 0 || U >= 16;
+  constexpr int kW = U >= 16 ? 16 : 8;
+  constexpr bool kP = U == 0 || U == 17;
   if (pow2_at_most_one(inv)) {   // inv = 1/(N S sigma) a power of two (N a power of two)
-    if constexpr (kPipe) rs_body_pipe<DT, kR32, NR, 2>(a, inv, sumsq, flag);
+    if constexpr (kG) rs_body_g<DT, kR32, NR, 2, kW, kP>(a, inv, sumsq, flag);
     else rs_body<DT, kR32, kReduce, kVec, NR, U, 2>(a, inv, sumsq, flag);
     flag = isfinite(sumsq) ? 0u : 1u;     // G^2 / b^2 of finite values are finite in fp64
     sumsq *= (double)inv * (double)inv;   // exact
   } else {
-    if constexpr (kPipe) rs_body_pipe<DT, kR32, NR, 1>(a, inv, sumsq, flag);
+    if constexpr (kG) rs_body_g<DT, kR32, NR, 1, kW, kP>(a, inv, sumsq, flag);
     else rs_body<DT, kR32, kReduce, kVec, NR, U, 1>(a, inv, sumsq, flag);
   }
   if (!a.cta_sum) {
@@ -1158,8 +1213,12 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
 
 template <int DT, bool R32, bool RED, int NR>
 cudaError_t launch_rs_u(const RSArgs& a, int grid, cudaStream_t s, int u) {
-  if (a.pipe) {
-    k_reduce_scatter<DT, R32, RED, true, NR, 0><<<grid, kThreads, 0, s>>>(a);
+  if (a.pipe) {   // 1: pipelined 128-bit; 2: 256-bit loads; 3: pipelined 256-bit
+    switch (a.pipe) {
+      case 2: k_reduce_scatter<DT, R32, RED, true, NR, 16><<<grid, kThreads, 0, s>>>(a); break;
+      case 3: k_reduce_scatter<DT, R32, RED, true, NR, 17><<<grid, kThreads, 0, s>>>(a); break;
+      default: k_reduce_scatter<DT, R32, RED, true, NR, 0><<<grid, kThreads, 0, s>>>(a); break;
+    }
     return cudaGetLastError();
   }
   switch (u) {
@@ -1187,10 +1246,16 @@ cudaError_t launch_rs_n(const RSArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s) {
+cudaError_t launch_reduce_scatter(const RSArgs& a_in, int grid, cudaStream_t s) {
+  RSArgs a = a_in;
   bool vec = aligned(a.dst, a.r32 ? 32 : 16);
   if (a.reduce)
     for (int r = 0; r < a.n; ++r) vec = vec && aligned(a.src[r], 16);
+  if (a.pipe >= 2) {   // 256-bit accesses need 32-B aligned sources and destination
+    bool v32 = aligned(a.dst, 32);
+    for (int r = 0; r < a.n; ++r) v32 = v32 && aligned(a.src[r], 32);
+    if (!v32) a.pipe = 1;
+  }
 #define ZRV(DT, R32, RED) return vec ? launch_rs_n<DT, R32, RED, true>(a, grid, s) : launch_rs_n<DT, R32, RED, false>(a, grid, s)
 #define ZRR(DT, R32) do { if (a.reduce) ZRV(DT, R32, true); else ZRV(DT, R32, false); } while (0)
   if (a.dtype == DT_F16) { if (a.r32) ZRR(DT_F16, true); else ZRR(DT_F16, false); }
@@ -1357,6 +1422,14 @@ __device__ void decide_apply(double sum, double flags, DevState* st, const Decid
   st->rec_clip = clip;
   st->rec_pad = 0;
   st->rec_norm = norm;
+  if (p.rec_out) {   // the caller's pinned record, written over PCIe (no D2H copy in the step)
+    uint64_t* r = reinterpret_cast<uint64_t*>(p.rec_out);
+    r[0] = st->t;
+    r[1] = (uint64_t)(overflow ? 1u : 0u) | ((uint64_t)__float_as_uint(S_used) << 32);
+    r[2] = (uint64_t)__float_as_uint(clip);
+    r[3] = (uint64_t)__double_as_longlong(norm);
+    __threadfence_system();
+  }
 }
 
 __global__ void k_decide_global(const __grid_constant__ PartialPtrs pp, DevState* st, const DecideParams p) {

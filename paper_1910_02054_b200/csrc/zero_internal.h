@@ -59,6 +59,7 @@ struct DecideParams {
   int dynamic;
   float beta1, beta2, lr, max_norm, min_scale, sigma;
   uint32_t window;
+  void* rec_out;            // device-visible pinned host copy of the step record (zero_step_info), or NULL
 };
 
 struct FlatPiece {

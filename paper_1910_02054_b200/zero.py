@@ -314,6 +314,7 @@ class ZeroEngine:
             ptrs.append(t.data_ptr() if t is not None else None)
         _check(lib.zero_bind_buffers(self._ctx, C.byref(CBuffers(*ptrs))), self._ctx)
         self._info_host = torch.empty(C.sizeof(CStepInfo), dtype=torch.uint8, pin_memory=True)
+        self._info_ptr = C.cast(C.c_void_p(self._info_host.data_ptr()), C.POINTER(CStepInfo))
 
     def destroy(self):
         if getattr(self, "_ctx", None):
@@ -375,8 +376,7 @@ class ZeroEngine:
 
     def step(self):
         """Enqueue zero_step; the record lands in pinned memory (read with step_info())."""
-        p = C.cast(C.c_void_p(self._info_host.data_ptr()), C.POINTER(CStepInfo))
-        _check(lib.zero_step(self._ctx, p), self._ctx)
+        _check(lib.zero_step(self._ctx, self._info_ptr), self._ctx)
 
     def step_begin(self):
         """zero_step_begin (ZeRO x MP): the step up to the decision; the DP-combined
@@ -385,8 +385,7 @@ class ZeroEngine:
 
     def step_end(self):
         """zero_step_end: decide from the (MP-all-reduced) partial and finish the step."""
-        p = C.cast(C.c_void_p(self._info_host.data_ptr()), C.POINTER(CStepInfo))
-        _check(lib.zero_step_end(self._ctx, p), self._ctx)
+        _check(lib.zero_step_end(self._ctx, self._info_ptr), self._ctx)
 
     def decision_partial(self) -> torch.Tensor:
         """float64[2] view {sum of squares, overflow count} of the partial zero_step_begin

@@ -9,16 +9,17 @@ Activations and the model's own gradient tensors are not counted (the paper's
 Table 2 counts model states).
 
   python scripts/max_model.py [--mem-gb 180] [--hidden 8192]      # host arithmetic through the C ABI
-  python scripts/max_model.py --device [--reserve-gb 4]           # validated on the GPU
+  python scripts/max_model.py --device [--slack-gb 0.05]           # validated on the GPU
 
 --device (rank 0's context of every (N_d, stage) cell, on this GPU): the budget is
-the device's free memory minus a reserve for the loader's temporary fp32 tensor;
+the device's free memory minus the loader's temporary (the fp32 masters of its
+largest chunk, <= max(2^28 elements, the largest tensor)) and 50 MB of slack;
 for the predicted L_max it runs zero_init, zero_buffer_sizes, allocates and binds
 the arenas (zeroed on the device) and loads the fp32 masters tensor by tensor
 (zero_load_master with NULL for the others: bounded temporary memory), then reads
 back zero_query(MEMORY) and checks a sample of the shard against the generator;
-with L_max + 1 blocks the arena allocation must fail with an out-of-memory error
-and leave the device usable.  Config 4 (60B = 75 x 8192, stage 3, N_d = 8) is
+with L_max + 1 blocks the arenas plus that temporary must fail to allocate with an
+out-of-memory error and leave the device usable.  Config 4 (60B = 75 x 8192, stage 3, N_d = 8) is
 instantiated the same way.  N_d > 1 cells build an unlinked PEER context: its
 arenas are exactly a real rank's (no step runs without its peers).
 """
@@ -62,6 +63,25 @@ def max_layers(h, n, stage, mem):
     return lo
 
 
+def load_chunks(ts, limit_elems=1 << 28):
+    """Tensor index groups of <= max(limit, largest tensor) elements (bounded temporary)."""
+    out, cur, n = [], [], 0
+    for i, t in enumerate(ts):
+        if cur and n + t.numel > limit_elems:
+            out.append(cur)
+            cur, n = [], 0
+        cur.append(i)
+        n += t.numel
+    if cur:
+        out.append(cur)
+    return out
+
+
+def loader_temp_bytes(h):
+    ts = synth.gpt_layout(1, h, 50257, 1024)
+    return 4 * max(max(t.numel for t in ts), 1 << 28)
+
+
 def instantiate(L, h, n, stage, load=True):
     """Rank 0's context of the L-block model on this GPU: arenas bound and (optionally)
     the fp32 masters loaded one tensor at a time.  Returns a result dict."""
@@ -76,16 +96,11 @@ def instantiate(L, h, n, stage, load=True):
     torch.cuda.synchronize()
     out = {"arena_bytes": sum(a.numel() for a in e.arenas.values() if a is not None)}
     if load:
-        chunk, cur = [], 0            # <= ~1 GB of fp32 masters per call (one tensor may be larger)
-        for i, t in enumerate(ts):
-            chunk.append(i)
-            cur += t.numel
-            if cur >= (1 << 28) or i == len(ts) - 1:
-                m = synth.gpu_masters(ts, 1, dev, only=set(chunk))
-                e.load_master(m)
-                torch.cuda.synchronize()
-                del m
-                chunk, cur = [], 0
+        for chunk in load_chunks(ts):   # the loader's temporary: <= LOADER_TEMP_BYTES of fp32 masters
+            m = synth.gpu_masters(ts, 1, dev, only=set(chunk))
+            e.load_master(m)
+            torch.cuda.synchronize()
+            del m
         # spot check: the first element this rank owns of the first bucket = the generator's value
         p32 = e.shard()[0]
         b0 = e.buckets[0]
@@ -105,13 +120,22 @@ def instantiate(L, h, n, stage, load=True):
 
 
 def over_the_top(L, h, n, stage):
-    """L blocks must not fit: the arena allocation fails with an OOM and the device stays usable."""
+    """L blocks must not fit: the arenas plus the loader's temporary cannot be allocated
+    (an OOM, raised cleanly), and the device stays usable."""
     import torch
+    from paper_1910_02054_b200 import ZeroConfig
+    ts = synth.gpt_layout(L, h, 50257, 1024)
+    e = tmp = None
     try:
-        instantiate(L, h, n, stage, load=False)
+        e = ZeroEngine([t.numel for t in ts], [t.layer for t in ts], n, 0, stage, ZeroConfig.defaults("bf16"),
+                       transport="local" if n == 1 else "peer", bucket_cap=1 << 26, device=torch.device("cuda", 0))
+        tmp = torch.empty(loader_temp_bytes(h), dtype=torch.uint8, device="cuda")
         res = "fit (unexpected)"
     except torch.OutOfMemoryError:
         res = "out of memory"
+    if e is not None:
+        e.destroy()
+    del e, tmp
     gc.collect()
     torch.cuda.empty_cache()
     x = torch.ones(1 << 20, device="cuda")          # the device is still usable
@@ -124,9 +148,13 @@ def device_main(args):
     import torch
     torch.cuda.init()
     free, total = torch.cuda.mem_get_info()
-    budget = free - int(args.reserve_gb * 1e9)
+    # the budget for the arenas: the free memory minus the loader's temporary (fp32 masters of
+    # the largest load chunk) and a small allowance for the allocator's rounding
+    reserve = loader_temp_bytes(args.hidden) + int(args.slack_gb * 1e9)
+    budget = free - reserve
     print(json.dumps({"device": torch.cuda.get_device_name(0), "free_bytes": free, "total_bytes": total,
-                      "budget_bytes": budget, "reserve_gb": args.reserve_gb}), flush=True)
+                      "budget_bytes": budget, "loader_temp_bytes": loader_temp_bytes(args.hidden),
+                      "slack_gb": args.slack_gb}), flush=True)
     cells = [(1, s) for s in (0, 1, 2, 3)] + [(n, s) for n in (2, 4, 8) for s in (1, 2, 3)]
     for n, stage in cells:
         L = max_layers(args.hidden, n, stage, budget)
@@ -155,7 +183,7 @@ def main():
     ap.add_argument("--mem-gb", type=float, default=180.0)
     ap.add_argument("--hidden", type=int, default=8192)
     ap.add_argument("--device", action="store_true")
-    ap.add_argument("--reserve-gb", type=float, default=4.0)
+    ap.add_argument("--slack-gb", type=float, default=0.05)
     args = ap.parse_args()
     if args.device:
         return device_main(args)
