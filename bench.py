@@ -74,6 +74,10 @@ def parse():
     ap.add_argument("--allow-unverified", action="store_true",
                     help="run a transport without a passing multi-device parity test (the line says so)")
     ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--phase-events", default="auto", choices=["auto", "on", "off"],
+                    help="library phase events inside the timed region (auto: on unless the model is < 1e8 "
+                         "params, where their host cost is visible; the phase split then comes from a separate "
+                         "instrumented pass)")
     ap.add_argument("--graph", action="store_true",
                     help="capture one whole step (all zero_reduce_grads + zero_step) in a CUDA graph and time replays")
     ap.add_argument("--no-e2e", action="store_true")
@@ -465,6 +469,10 @@ def main():
         barrier()
         torch.cuda.synchronize()
         comm1 = eng.comm_counters()
+        in_region = graph is None and (args.phase_events == "on" or
+                                       (args.phase_events == "auto" and psi_total >= 100_000_000))
+        if graph is None and not in_region:
+            eng.set_timing(False)
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
         if clocks:
             clocks.mark(True)
@@ -482,6 +490,15 @@ def main():
         clk = clocks.stop() if clocks else None
         tm = eng.timing()
         launches = tm.kernel_launches - launches0 if graph is None else launches_per_step * steps
+        phase_events = "in the timed region" if in_region else None
+        if graph is None and not in_region:    # the phase split from a separate instrumented pass
+            eng.set_timing(True)
+            n_instr = min(steps, 20)
+            for _ in range(n_instr):
+                one_step()
+            torch.cuda.synchronize()
+            tm = eng.timing()
+            phase_events = f"a separate instrumented pass of {n_instr} steps (none in the timed region)"
         phases = None
         if args.stage == 3 and graph is None:
             # one more (untimed) step with events on the caller's stream: with no model compute
@@ -500,7 +517,7 @@ def main():
         else:   # replays do not pass through the host counters: the captured step's counts
             sent = [getattr(comm1, f) - getattr(comm0, f) for f in ("reduce_scatter", "all_gather", "all_reduce")]
         return {"ms": ms, "per_step": per_step, "tm": tm, "launches": launches, "clocks": clk, "rec": rec,
-                "graph": graph is not None, "sent": sent, "phases": phases}
+                "graph": graph is not None, "sent": sent, "phases": phases, "phase_events": phase_events}
 
     eng, cfg, grad_buf, grads = build(args.dtype)
     info = eng.info
@@ -594,6 +611,7 @@ def main():
                      "frac": adam_gbs / hbm_peak if adam_gbs else None, "traffic": traffic,
                      "bytes_per_launch": adam_bytes, "ms_per_launch": adam_ms,
                      "share_of_step": adam_ms / ms if adam_ms else None,
+                     "events": res["phase_events"],
                      "note": None if adam_ms else "--graph: per-kernel events are not recorded inside the graph"},
         "step_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
                           "hbm_gbs": hbm_peak, "nvlink_gbs": NVLINK_GBS if N > 1 else None,

@@ -38,7 +38,7 @@ extern "C" {
 #endif
 
 #define ZERO_ABI_VERSION 3     /* 2: zero_config.mp_rank, zero_tensor.flags, zero_step_begin/end, zero_pa_*;
-                                  3: zero_timing.ag_ms, R32 over NCCL, zero_wait (NCCL watchdog) */
+                                  3: zero_timing.ag_ms, R32 over NCCL, zero_wait (NCCL watchdog), zero_set_timing */
 #define ZERO_MAX_RANKS 8      /* one NVL8 box */
 
 typedef enum {
@@ -382,6 +382,10 @@ typedef struct {          /* device time per phase, CUDA events on the launching
   uint64_t adam_launches;
 } zero_timing;
 zero_status zero_query(const struct zero_ctx* ctx, int what, void* out, size_t out_bytes);
+/* Turn the per-phase CUDA events of ZERO_Q_TIMING on (1) or off (0) from the next step on
+ * (zero_config.timing sets the initial state).  Host-only; ZERO_ESTATE inside a step (after
+ * its first zero_reduce_grads). */
+zero_status zero_set_timing(struct zero_ctx* ctx, int on);
 
 /* Last error text of ctx (NULL: of the calling thread's last failed zero_init or
  * zero_plan_layout).  The string is owned by the library and valid until the next

@@ -2057,6 +2057,13 @@ zero_status zero_wait(zero_ctx* c, uint64_t timeout_ms) {
   }
 }
 
+zero_status zero_set_timing(zero_ctx* c, int on) {
+  STICKY(c);
+  if (c->step_open || c->n_reduced) return c->fail(ZERO_ESTATE, "zero_set_timing inside a step");
+  c->cfg.timing = on ? 1u : 0u;
+  return ZERO_OK;
+}
+
 const char* zero_last_error(const zero_ctx* c) {
   if (!c) return g_init_error.c_str();
   return c->err.c_str();

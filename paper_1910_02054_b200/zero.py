@@ -104,7 +104,8 @@ EXPORTS = ["zero_plan_layout", "zero_init", "zero_buffer_sizes", "zero_bind_buff
            "zero_peer_export", "zero_peer_open", "zero_export_state", "zero_import_state",
            "zero_load_master", "zero_set_grad_ptrs", "zero_reduce_grads", "zero_step", "zero_step_begin",
            "zero_step_end", "zero_gather_params",
-           "zero_release_params", "zero_param_view", "zero_query", "zero_last_error", "zero_wait", "zero_destroy",
+           "zero_release_params", "zero_param_view", "zero_query", "zero_set_timing", "zero_last_error", "zero_wait",
+           "zero_destroy",
            "zero_model_state_bytes", "zero_comm_elems_per_rank", "zero_abi_version",
            "zero_pa_init", "zero_pa_get_info", "zero_pa_bind", "zero_pa_sim_group", "zero_pa_save",
            "zero_pa_prefetch", "zero_pa_gather", "zero_pa_get_counters", "zero_pa_last_error", "zero_pa_destroy",
@@ -141,6 +142,7 @@ def _load():
         "zero_query": ([P, C.c_int, P, C.c_size_t], C.c_int),
         "zero_last_error": ([P], C.c_char_p),
         "zero_wait": ([P, C.c_uint64], C.c_int),
+        "zero_set_timing": ([P, C.c_int], C.c_int),
         "zero_destroy": ([P], None),
         "zero_model_state_bytes": ([C.c_uint64, C.c_int, C.c_int, C.c_int], C.c_uint64),
         "zero_comm_elems_per_rank": ([C.c_uint64, C.c_int, C.c_int], C.c_uint64),
@@ -479,6 +481,10 @@ class ZeroEngine:
         out = CComm()
         _check(lib.zero_query(self._ctx, Q_COMM, C.byref(out), C.sizeof(out)), self._ctx)
         return out
+
+    def set_timing(self, on: bool):
+        """zero_set_timing: per-phase CUDA events on / off from the next step."""
+        _check(lib.zero_set_timing(self._ctx, 1 if on else 0), self._ctx)
 
     def timing(self) -> CTiming:
         """Phase times accumulated since the last call (needs config.timing)."""

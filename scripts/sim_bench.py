@@ -40,7 +40,14 @@ def main():
         e.set_grads(grads[r])
     nb = grp[0].info.n_buckets
 
+    layers = sorted({b.layer for b in grp[0].buckets})
+
     def step():
+        if args.stage == 3:   # the forward's layer gathers (k_copy pulls of every rank's shard slice)
+            for L in layers:
+                for e in grp.ranks:
+                    e.gather_params(L)
+                    e.release_params(L)
         for k in reversed(range(nb)):
             for e in grp.ranks:
                 e.reduce_grads(k)
@@ -65,7 +72,10 @@ def main():
     # HBM bytes of one simulated step (all ranks on this GPU)
     flat = 4 * pp * N                                   # every rank flattens its Psi'
     rs = N * (N * 2 * pp / N + 2 * pp / N)              # each rank reads N slices, writes its reduced slice
-    adam = N * 28 * pp / N + (N - 1) * 2 * pp           # K=12 state + G + own p16, plus the other replicas' stores
+    if args.stage == 3:                                 # own shard's p16 only; + every rank gathers Psi' (read + write)
+        adam = N * 28 * pp / N + N * 4 * pp
+    else:
+        adam = N * 28 * pp / N + (N - 1) * 2 * pp       # K=12 state + G + own p16, plus the other replicas' stores
     print(json.dumps({"bench": "sim_step", "ranks": N, "stage": args.stage, "psi_padded": pp,
                       "ms_per_step": ms, "hbm_bytes_per_step": flat + rs + adam,
                       "effective_TBps": (flat + rs + adam) / (ms * 1e-3) / 1e12,
