@@ -201,7 +201,7 @@ struct zero_ctx {
   bool flat_cta_partials = true;                   // ZERO_FLAT_CTA_PARTIALS=0: last-CTA combine in each flatten
   bool rs_cta_partials = true;                     // ZERO_RS_CTA_PARTIALS=0: last-CTA combine in each reduce-scatter
   int rs_ctas = 4, rs_u = 0;                       // ZERO_RS_CTAS (CTAs per SM), ZERO_RS_U (0 = per-N default)
-  int rs_pipe = 0;                                 // ZERO_RS_PIPE: the software-pipelined pull
+  int rs_pipe = 1;                                 // ZERO_RS_PIPE: 1 = software-pipelined pull (default), 0 = plain
   // ZeRO x MP (R-MP1): per-slot norm weights (0 for MP-replicated buckets on MP rank > 0)
   double* slot_w = nullptr;
   std::vector<double> slot_w_host;
@@ -784,6 +784,7 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   }
   if (const char* ev = getenv("ZERO_FLAT_CTA_PARTIALS")) c->flat_cta_partials = atoi(ev) != 0;
   if (const char* ev = getenv("ZERO_RS_CTA_PARTIALS")) c->rs_cta_partials = atoi(ev) != 0;
+  c->rs_ctas = c->n_d == 8 ? 3 : 4;   // the pipelined pull at N_d = 8 holds 78 registers: 3 CTAs/SM
   if (const char* ev = getenv("ZERO_RS_CTAS")) c->rs_ctas = std::max(1, std::min(8, atoi(ev)));
   if (const char* ev = getenv("ZERO_RS_U")) c->rs_u = atoi(ev);
   if (const char* ev = getenv("ZERO_RS_PIPE")) c->rs_pipe = atoi(ev);
@@ -1067,7 +1068,7 @@ bool batchable(const zero_ctx* c, uint32_t k) {
 // one launch for the pending run of adjacent small buckets [pend_lo, pend_hi] (N_d = 1): their
 // pieces tile [base_lo, base_hi + B_hi) contiguously; the epilogue partials go to the first
 // bucket's slot and the run's other slots are cleared
-zero_status flush_small(zero_ctx* c, bool on_caller_stream = false) {
+zero_status flush_small(zero_ctx* c, bool on_caller_stream = false, bool* decided = nullptr, void* rec_dev = nullptr) {
   if (c->pend_lo < 0) return ZERO_OK;
   std::stable_sort(c->pend_pieces.begin(), c->pend_pieces.end(),
                    [](const std::pair<uint32_t, FlatPiece>& x, const std::pair<uint32_t, FlatPiece>& y) {
@@ -1102,6 +1103,15 @@ zero_status flush_small(zero_ctx* c, bool on_caller_stream = false) {
   a.cta_flag = c->cta_flag + (size_t)slot * kMaxGrid;
   a.cta_grid = c->cta_grid + slot;
   a.clear_slots = (uint32_t)(c->slot_base[hi] - slot);   // one slot per batchable bucket
+  // the whole step in this launch (zero_step, a small model): its last CTA also decides
+  if (decided && lo == 0 && hi + 1 == c->info.n_buckets && c->n_slots == (int)c->info.n_buckets) {
+    a.decide_st = c->st;
+    a.decide_out = c->my_partial;
+    a.decide_part = c->part_comm;
+    a.decide = decide_params(c);
+    a.decide.rec_out = rec_dev;
+    *decided = true;
+  }
   CK(launch_flatten(a, grid, fs, c->flat_vecs));
   c->launches++;
   c->pend_lo = c->pend_hi = -1;
@@ -1137,9 +1147,9 @@ zero_status defer_small(zero_ctx* c, uint32_t k, const void* const* grads) {
 }
 
 // pull reduce-scatter of bucket k for rank c (PEER), sources = every member's flattened bucket
-zero_status issue_pull_rs(zero_ctx* c, ZeroGroup* g, uint32_t k) {
+int fill_pull_rs(zero_ctx* c, ZeroGroup* g, uint32_t k, RSArgs& a) {
   const uint64_t sl = c->slice(k);
-  RSArgs a{};
+  a = RSArgs{};
   for (int j = 0; j < g->n; ++j) a.src[j] = g->ranks[j]->flat_dst(k) + (uint64_t)c->rank * sl;
   a.dst = c->rs_dst(k);
   a.count = sl;
@@ -1150,9 +1160,33 @@ zero_status issue_pull_rs(zero_ctx* c, ZeroGroup* g, uint32_t k) {
   a.st = c->st;
   a.part = c->part_comm;
   a.slot = c->slots + c->slot_base[k];
-  CK(launch_reduce_scatter(a, rs_setup(c, k, a, sl), c->comm_stream));
-  c->launches++;
-  c->counters.reduce_scatter += sl * (uint64_t)(c->n_d - 1);
+  return rs_setup(c, k, a, sl);
+}
+
+// simulated ranks: every rank's pull of bucket k in one launch (they share the stream and run
+// concurrently, as they would on separate GPUs); per-rank launches when not eligible
+zero_status issue_pull_rs_all(ZeroGroup* g, uint32_t k) {
+  RSMulti m{};
+  m.n = g->n;
+  int grid = 0;
+  for (int j = 0; j < g->n; ++j) grid = fill_pull_rs(g->ranks[j], g, k, m.r[j]);
+  zero_ctx* c = g->ranks[0];
+  const cudaError_t e = launch_reduce_scatter_multi(m, grid, c->comm_stream);
+  if (e == cudaSuccess) {
+    c->launches++;
+  } else if (e == cudaErrorNotSupported) {
+    cudaGetLastError();
+    for (int j = 0; j < g->n; ++j) {
+      zero_ctx* cj = g->ranks[j];
+      if (launch_reduce_scatter(m.r[j], grid, cj->comm_stream) != cudaSuccess)
+        return cj->fail(ZERO_ECUDA, "pull reduce-scatter launch failed");
+      cj->launches++;
+    }
+  } else {
+    return c->fail(ZERO_ECUDA, "pull reduce-scatter launch failed: %s", cudaGetErrorString(e));
+  }
+  for (int j = 0; j < g->n; ++j)
+    g->ranks[j]->counters.reduce_scatter += g->ranks[j]->slice(k) * (uint64_t)(g->n - 1);
   return ZERO_OK;
 }
 
@@ -1275,10 +1309,8 @@ zero_status zero_reduce_grads(zero_ctx* c, uint32_t k, const void* const* tensor
     if (pooled) c->pool_pending[ps] = (int)k;
     c->reduced[k] = 1;  // this rank's part is done; the collective completes below
     if (++g->flat_count[k] == g->n) {
-      for (int j = 0; j < g->n; ++j) {
-        zero_status r = issue_pull_rs(g->ranks[j], g, k);
-        if (r != ZERO_OK) return r;
-      }
+      zero_status r = issue_pull_rs_all(g, k);
+      if (r != ZERO_OK) return r;
       if (c->stage == 0) {  // all-reduce = RS + AG of the reduced slices
         for (int j = 0; j < g->n; ++j) {
           zero_ctx* cj = g->ranks[j];
@@ -1433,7 +1465,7 @@ zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev,
   }
 
   // the pending run of small buckets (N_d = 1), on the caller's stream: the step follows it there
-  if (zero_status s = flush_small(c, true)) return s;
+  if (zero_status s = flush_small(c, true, decided, rec_dev)) return s;
   if (c->gather_stream) {  // no rank's Adam may rewrite a shard a gather still reads
     CK(cudaEventRecord(c->ev_gjoin, c->gather_stream));
     CK(cudaStreamWaitEvent(c->comm_stream, c->ev_gjoin, 0));
@@ -1452,7 +1484,8 @@ zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev,
   }
   pp = PartialPtrs{};
   if (c->transport == ZERO_TRANSPORT_LOCAL) {
-    CK(issue_decide_local(c, c->comm_stream, decided, rec_dev));   // the flattens left per-CTA partials
+    if (!(decided && *decided))   // (else the whole-step flatten already decided)
+      CK(issue_decide_local(c, c->comm_stream, decided, rec_dev));   // the flattens left per-CTA partials
     pp.p[0] = c->my_partial;
     pp.n = 1;
   } else if (c->ipc) {  // push my partial into every peer's gathered[rank], then wait for all

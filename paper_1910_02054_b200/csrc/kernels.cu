@@ -247,6 +247,35 @@ __device__ void grid_publish(double s, uint32_t f, GridPartials* part, Slot* slo
   }
 }
 
+__device__ void decide_apply(double sum, double flags, DevState* st, const DecideParams& p);
+
+// the last CTA of a whole-step flatten (N_d = 1, every bucket in one launch): sum the per-CTA
+// partials in CTA order and make the decision -- k_decide_local_slots + k_decide_global fused
+__device__ __noinline__ void flat_decide(const FlatArgs& a) {
+  __shared__ bool is_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    is_last = atomicAdd(&a.decide_part->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double s = 0.0;
+  uint32_t f = 0;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+    s += __ldcg(&a.cta_sum[i]);
+    f |= __ldcg(&a.cta_flag[i]);
+  }
+  block_reduce(s, f);
+  if (threadIdx.x == 0) {
+    a.decide_part->ticket = 0;
+    a.decide_out->sumsq = s;
+    a.decide_out->flag = f ? 1.0 : 0.0;
+    decide_apply(s, f ? 1.0 : 0.0, a.decide_st, a.decide);
+  }
+}
+
 // the flatten's N_d = 1 epilogue: per-CTA partials (k_decide_local combines them in a
 // fixed order), or the last-CTA grid combine into the slot
 __device__ __forceinline__ void flat_publish(const FlatArgs& a, double s, uint32_t f) {
@@ -259,6 +288,7 @@ __device__ __forceinline__ void flat_publish(const FlatArgs& a, double s, uint32
     }
     if (blockIdx.x == 0)
       for (uint32_t i = threadIdx.x; i < a.clear_slots; i += blockDim.x) a.cta_grid[1 + i] = 0u;
+    if (a.decide_st) flat_decide(a);
   } else {
     grid_publish(s, f, a.part, a.slot);
   }
@@ -1166,7 +1196,7 @@ __device__ __forceinline__ void rs_body_g(const RSArgs& a, float inv, double& su
 }
 
 template <int DT, bool kR32, bool kReduce, bool kVec, int NR, int U>
-__global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_constant__ RSArgs a) {
+__device__ __forceinline__ void rs_main(const RSArgs& a) {
   if (a.wait_flags) {  // every rank has flattened this bucket (cross-process PEER)
     if (threadIdx.x == 0) wait_all(a.wait_flags, a.n, a.epoch);
     __syncthreads();
@@ -1209,6 +1239,43 @@ __global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_consta
     __threadfence_system();
     for (int j = 0; j < a.n; ++j) st_release_sys(a.done_sig[j], a.epoch);
   }
+}
+
+template <int DT, bool kR32, bool kReduce, bool kVec, int NR, int U>
+__global__ void __launch_bounds__(kThreads) k_reduce_scatter(const __grid_constant__ RSArgs a) {
+  rs_main<DT, kR32, kReduce, kVec, NR, U>(a);
+}
+
+// simulated ranks (one process, one GPU): the pull reduce-scatters of every rank for one
+// bucket in one launch, grid row y = rank y -- they run concurrently, as on an NVL8 box
+template <int DT, bool kR32, int NR>
+__global__ void __launch_bounds__(kThreads) k_reduce_scatter_multi(const __grid_constant__ RSMulti m) {
+  rs_main<DT, kR32, true, true, NR, 0>(m.r[blockIdx.y]);
+}
+
+cudaError_t launch_reduce_scatter_multi(const RSMulti& m, int grid, cudaStream_t s) {
+  const RSArgs& a0 = m.r[0];
+  for (int i = 0; i < m.n; ++i) {
+    const RSArgs& a = m.r[i];
+    if (!a.reduce || !a.pipe || a.wait_flags || a.n != a0.n || a.dtype != a0.dtype || a.r32 != a0.r32 ||
+        !aligned(a.dst, a.r32 ? 32 : 16))
+      return cudaErrorNotSupported;
+    for (int r = 0; r < a.n; ++r)
+      if (!aligned(a.src[r], 16)) return cudaErrorNotSupported;
+  }
+  const dim3 g(grid, m.n);
+#define ZM(DT, R32)                                                                          \
+  switch (a0.n) {                                                                            \
+    case 2: k_reduce_scatter_multi<DT, R32, 2><<<g, kThreads, 0, s>>>(m); break;           \
+    case 4: k_reduce_scatter_multi<DT, R32, 4><<<g, kThreads, 0, s>>>(m); break;           \
+    case 8: k_reduce_scatter_multi<DT, R32, 8><<<g, kThreads, 0, s>>>(m); break;           \
+    default: return cudaErrorNotSupported;                                                   \
+  }
+  if (a0.dtype == DT_F16) { if (a0.r32) { ZM(DT_F16, true) } else { ZM(DT_F16, false) } }
+  else if (a0.dtype == DT_BF16) { if (a0.r32) { ZM(DT_BF16, true) } else { ZM(DT_BF16, false) } }
+  else return cudaErrorNotSupported;
+#undef ZM
+  return cudaGetLastError();
 }
 
 template <int DT, bool R32, bool RED, int NR>

@@ -87,6 +87,12 @@ struct FlatArgs {
   uint32_t clear_slots;     // batched small buckets: the next clear_slots slots' cta_grid := 0 (their
                             // elements' partials are this launch's, in cta_grid[0]'s slot)
   int pdl;                  // host: launch as a programmatic dependent of the previous flatten
+  // N_d = 1, one launch holding every bucket of the step (a small model): its last CTA
+  // combines the per-CTA partials (CTA order) and makes the step's decision (decide_st != NULL)
+  DevState* decide_st;
+  RankPartial* decide_out;
+  GridPartials* decide_part;    // ticket
+  DecideParams decide;
 };
 
 struct RSArgs {
@@ -113,6 +119,11 @@ struct RSArgs {
   uint32_t* cta_grid;
   int u;                        // host: 8-element groups per thread per iteration (0 = default)
   int pipe;                     // host: software-pipelined variant (next group's loads in flight)
+};
+
+struct RSMulti {                // every simulated rank's pull reduce-scatter of one bucket
+  RSArgs r[kMaxRanks];
+  int n;
 };
 
 struct AdamSeg {
@@ -172,6 +183,8 @@ cudaError_t launch_flatten_tma(const FlatArgs& a, int grid, cudaStream_t s, int 
 cudaError_t launch_flatten_wide(const FlatArgs& a, int grid, cudaStream_t s);
 int flatten_tma_ctas_per_sm(int variant);
 cudaError_t launch_reduce_scatter(const RSArgs& a, int grid, cudaStream_t s);
+// cudaErrorNotSupported: not eligible (the caller launches per rank instead)
+cudaError_t launch_reduce_scatter_multi(const RSMulti& m, int grid, cudaStream_t s);
 // cta_*: optional per-CTA flatten partials (N_d == 1), slot i at [i * kMaxGrid, + cta_grid[i])
 // slot_w: optional per-slot norm weights (0 or 1; ZeRO x MP, R-MP1)
 cudaError_t launch_decide_local(Slot* slots, int n_slots, RankPartial* out, cudaStream_t s,

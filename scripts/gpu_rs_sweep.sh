@@ -12,9 +12,8 @@ run() {  # ranks, name, env...
       python scripts/sim_bench.py --ranks $n --stage 2 --config gpt2_1.5b_l8 --steps 2 > gpurun_out/rs_sweep/n${n}_$name.log 2>&1
 }
 for n in ${RS_RANKS:-2 4 8}; do
-  run $n u2_c4 ZERO_RS_CTAS=4 ZERO_RS_U=2
-  run $n u1_c4 ZERO_RS_CTAS=4 ZERO_RS_U=1
-  run $n u1_c6 ZERO_RS_CTAS=6 ZERO_RS_U=1
+  run $n plain_u2_c4 ZERO_RS_PIPE=0 ZERO_RS_CTAS=4 ZERO_RS_U=2
+  run $n plain_u1_c6 ZERO_RS_PIPE=0 ZERO_RS_CTAS=6 ZERO_RS_U=1
   run $n pipe_c4 ZERO_RS_CTAS=4 ZERO_RS_PIPE=1
   run $n pipe_c3 ZERO_RS_CTAS=3 ZERO_RS_PIPE=1
 done

@@ -9,11 +9,11 @@ Activations and the model's own gradient tensors are not counted (the paper's
 Table 2 counts model states).
 
   python scripts/max_model.py [--mem-gb 180] [--hidden 8192]      # host arithmetic through the C ABI
-  python scripts/max_model.py --device [--slack-gb 0.05]           # validated on the GPU
+  python scripts/max_model.py --device [--slack-gb 0.25]           # validated on the GPU
 
 --device (rank 0's context of every (N_d, stage) cell, on this GPU): the budget is
 the device's free memory minus the loader's temporary (the fp32 masters of its
-largest chunk, <= max(2^28 elements, the largest tensor)) and 50 MB of slack;
+largest chunk, <= max(2^28 elements, the largest tensor)) and 0.25 GB of slack;
 for the predicted L_max it runs zero_init, zero_buffer_sizes, allocates and binds
 the arenas (zeroed on the device) and loads the fp32 masters tensor by tensor
 (zero_load_master with NULL for the others: bounded temporary memory), then reads
@@ -183,7 +183,7 @@ def main():
     ap.add_argument("--mem-gb", type=float, default=180.0)
     ap.add_argument("--hidden", type=int, default=8192)
     ap.add_argument("--device", action="store_true")
-    ap.add_argument("--slack-gb", type=float, default=0.05)
+    ap.add_argument("--slack-gb", type=float, default=0.25)
     args = ap.parse_args()
     if args.device:
         return device_main(args)

@@ -5,8 +5,8 @@ held to the same bit-exact parity against the oracle as the defaults (test_gpu_p
   ZERO_ADAM_SMALL elements (every benchmarked model), while the small test layouts run the
   register-staged kernel; forced here on small and ragged shards;
 * the flatten without the batching of adjacent small buckets (ZERO_SMALL_BUCKET=0);
-* the reduce-scatter with a last-CTA combine instead of per-CTA partials, the
-  software-pipelined pull, and other loads-in-flight settings;
+* the reduce-scatter with a last-CTA combine instead of per-CTA partials, the plain
+  (not software-pipelined) pull with other loads-in-flight settings, 256-bit loads;
 * the flatten's last-CTA combine (ZERO_FLAT_CTA_PARTIALS=0).
 The knobs are environment variables read when the arenas are bound."""
 import pytest
@@ -25,8 +25,10 @@ VARIANTS = {
     "adam_tma": {"ZERO_ADAM_VARIANT": "21"},
     "adam_tma_no_batch": {"ZERO_ADAM_VARIANT": "21", "ZERO_SMALL_BUCKET": "0"},
     "rs_grid_combine": {"ZERO_RS_CTA_PARTIALS": "0"},
-    "rs_pipe": {"ZERO_RS_PIPE": "1", "ZERO_RS_CTAS": "2"},
-    "rs_u1_c6": {"ZERO_RS_U": "1", "ZERO_RS_CTAS": "6"},
+    "rs_plain_u2": {"ZERO_RS_PIPE": "0", "ZERO_RS_CTAS": "2"},
+    "rs_plain_u1_c6": {"ZERO_RS_PIPE": "0", "ZERO_RS_U": "1", "ZERO_RS_CTAS": "6"},
+    "rs_w16": {"ZERO_RS_PIPE": "2"},
+    "rs_w16_pipe": {"ZERO_RS_PIPE": "3", "ZERO_RS_CTAS": "2"},
     "flat_grid_combine": {"ZERO_FLAT_CTA_PARTIALS": "0", "ZERO_SMALL_BUCKET": "0"},
 }
 
