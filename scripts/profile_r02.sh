@@ -27,3 +27,6 @@ for r in adam flatten rs copy; do
   ncu -i $O/$r.ncu-rep --page raw --csv > $O/$r.raw.csv 2>/dev/null
   ncu -i $O/$r.ncu-rep --page details --csv > $O/$r.details.csv 2>/dev/null
 done
+# the .ncu-rep files are large: keep the CSV exports only (gpurun copies back <= 64 MiB)
+mkdir -p /tmp/ncu_reps && mv $O/*.ncu-rep /tmp/ncu_reps/ 2>/dev/null
+du -sh gpurun_out
