@@ -1171,7 +1171,8 @@ zero_status issue_pull_rs_all(ZeroGroup* g, uint32_t k) {
   int grid = 0;
   for (int j = 0; j < g->n; ++j) grid = fill_pull_rs(g->ranks[j], g, k, m.r[j]);
   zero_ctx* c = g->ranks[0];
-  const cudaError_t e = launch_reduce_scatter_multi(m, grid, c->comm_stream);
+  static const bool multi = !getenv("ZERO_RS_MULTI") || atoi(getenv("ZERO_RS_MULTI")) != 0;
+  const cudaError_t e = multi ? launch_reduce_scatter_multi(m, grid, c->comm_stream) : cudaErrorNotSupported;
   if (e == cudaSuccess) {
     c->launches++;
   } else if (e == cudaErrorNotSupported) {
