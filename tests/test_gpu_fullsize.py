@@ -1,6 +1,7 @@
 """Parity at BASELINE config 2's full size (GPT-2 1.5B layout, Psi = 1,557,611,200,
-stage 1, N_d = 1, bf16) in the launch configuration bench.py times, and at config
-3's (the paper's Fig. 1 7.5B model, Psi = 7.5e9, stage 2, N_d = 1: 135 GB of arenas).
+stage 1, N_d = 1, bf16) and at config 3's (the paper's Fig. 1 7.5B model, Psi = 7.5e9,
+stage 2, N_d = 1: 135 GB of arenas) in the launch configurations bench.py times: the
+contract line (bf16) and its fp16 key (dynamic loss scaling, gradients at S = 2^16).
 
 The oracle cannot hold 1.5B-element replicas, so (③) we compare on SAMPLED outputs
 the oracle computes one by one: with clipping off, Adam is elementwise, so the
@@ -23,14 +24,15 @@ if not torch.cuda.is_available():
     pytest.skip("needs a GPU", allow_module_level=True)
 
 
-@pytest.mark.parametrize("config,stage", [("gpt2_1.5b", 1), ("gpt_7.5b", 2)])
-def test_full_size_sampled(config, stage):
+@pytest.mark.parametrize("config,stage,dt", [("gpt2_1.5b", 1, "bf16"), ("gpt_7.5b", 2, "bf16"), ("gpt_7.5b", 2, "fp16")])
+def test_full_size_sampled(config, stage, dt):
     from paper_1910_02054_b200 import ZeroConfig, ZeroEngine
     torch.cuda.empty_cache()
     ts = synth.CONFIGS[config]()
     dev = torch.device("cuda", 0)
-    cfg = OS.AdamConfig.defaults("bf16")
-    eng = ZeroEngine([t.numel for t in ts], [t.layer for t in ts], 1, 0, stage, ZeroConfig.defaults("bf16"), "local",
+    cfg = OS.AdamConfig.defaults(dt)
+    S = float(cfg.loss_scale)                       # fp16: 2^16 (dynamic, no overflow here); bf16: 1
+    eng = ZeroEngine([t.numel for t in ts], [t.layer for t in ts], 1, 0, stage, ZeroConfig.defaults(dt), "local",
                      align=64, bucket_cap=1 << 26, device=dev)
     for i in range(len(ts)):                       # chunked master load (NULL = skip)
         masters = synth.gpu_masters(ts, 1, dev, only={i})
@@ -53,21 +55,23 @@ def test_full_size_sampled(config, stage):
     b1t = b2t = 1.0
     nb = eng.info.n_buckets
     for step in range(2):
-        buf, grads = synth.gpu_grads_flat(ts, 1, 0, step, torch.bfloat16, dev)
+        tdt = torch.bfloat16 if dt == "bf16" else torch.float16
+        buf, grads = synth.gpu_grads_flat(ts, 1, 0, step, tdt, dev, scale=S)
         for k in reversed(range(nb)):
             eng.reduce_grads(k, grads)
         eng.step()
         info = eng.step_info()
         ch = 1 << 27   # fp64 norm of the gradients in chunks (bounded temporary)
         ref_norm = math.sqrt(math.fsum(float(torch.linalg.vector_norm(buf[i:i + ch].double()) ** 2)
-                                       for i in range(0, buf.numel(), ch)))
+                                       for i in range(0, buf.numel(), ch))) / S    # norm of G / S (exact scaling)
         assert info.overflow == 0 and info.t == step + 1
         assert abs(info.grad_norm - ref_norm) <= 1e-12 * ref_norm
-        # oracle on the sampled elements (elementwise: c-3 with inv = 1, clip = 1)
+        assert info.loss_scale == S
+        # oracle on the sampled elements (elementwise: c-3 with inv = fp32(1/S), clip = 1)
         sc = np.float32(2.0) ** -(6 + (tid % 8)).astype(np.float32)
         u32 = synth.uniform_at(synth.stream_key(1, synth.KIND_GRAD, 0, step), samp) * sc
-        g16 = nx.to16(u32.astype(np.float32), "bf16")
-        G = nx.widen(g16, "bf16") * np.float32(1.0)
+        g16 = nx.to16((u32 * np.float32(S)).astype(np.float32), dt)
+        G = nx.widen(g16, dt) * np.float32(1.0 / S)
         b1t *= float(np.float32(cfg.beta1))
         b2t *= float(np.float32(cfg.beta2))
         step_f = np.float32(float(np.float32(cfg.lr)) / (1 - b1t))
@@ -87,7 +91,7 @@ def test_full_size_sampled(config, stage):
         bad = np.nonzero(got.view(np.uint32) != ref.view(np.uint32))[0]
         assert bad.size == 0, f"{name}: {bad.size} of {samp.size} sampled elements differ"
     p16 = eng.p16_arena()[fidx].cpu().view(torch.int16).numpy().view(np.uint16)
-    assert np.array_equal(p16, nx.to16(p, "bf16"))
+    assert np.array_equal(p16, nx.to16(p, dt))
     # the library's own memory accounting equals Fig. 1's (2+2+K) Psi' at N_d = 1
     mem = eng.memory()
     assert mem.params16 + mem.grads16 + mem.optimizer == 16 * eng.info.psi_padded
