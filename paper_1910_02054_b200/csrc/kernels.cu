@@ -1257,7 +1257,7 @@ cudaError_t launch_reduce_scatter_multi(const RSMulti& m, int grid, cudaStream_t
   const RSArgs& a0 = m.r[0];
   for (int i = 0; i < m.n; ++i) {
     const RSArgs& a = m.r[i];
-    if (!a.reduce || !a.pipe || a.wait_flags || a.n != a0.n || a.dtype != a0.dtype || a.r32 != a0.r32 ||
+    if (!a.reduce || a.pipe != 1 || a.wait_flags || a.n != a0.n || a.dtype != a0.dtype || a.r32 != a0.r32 ||
         !aligned(a.dst, a.r32 ? 32 : 16))
       return cudaErrorNotSupported;
     for (int r = 0; r < a.n; ++r)
