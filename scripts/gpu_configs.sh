@@ -17,6 +17,6 @@ done
 timeout 600 python bench.py --config gpt2_1.5b --stage 1 --dtype fp16 --steps 50 --no-cpu-baseline --no-e2e >> $O 2>> gpurun_out/configs.err
 timeout 600 python bench.py --config mlp1m --no-cpu-baseline --no-e2e --no-fp16-key >> $O 2>> gpurun_out/configs.err
 timeout 600 python bench.py --config mlp1m --graph --no-cpu-baseline --no-e2e >> $O 2>> gpurun_out/configs.err
-for opt in zero torch; do
+for opt in zero torch none; do
   timeout 900 python scripts/train_bench.py --opt $opt >> gpurun_out/train_bench.jsonl 2>> gpurun_out/train_bench.err
 done

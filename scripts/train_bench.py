@@ -9,7 +9,9 @@ zero_step runs the fused Adam into the parameters the model computes with.
 
 Baseline arm (--opt torch): the same model with a conventional mixed-precision
 optimizer in plain torch (fp32 master copy, torch.optim.Adam(fused=True), bf16
-copy-back), i.e. what the library replaces.
+copy-back), i.e. what the library replaces.  --opt none: forward + backward alone;
+(T_zero - T_none) / T_zero is the exposed fraction of the ZeRO work (flattens hidden in
+backward or not, plus the step).
 
   python scripts/train_bench.py [--layers 48 --hidden 1600 --batch 8 --seq 1024] [--opt zero|torch]
 """
@@ -70,7 +72,8 @@ def main():
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--opt", default="zero", choices=["zero", "torch"])
+    ap.add_argument("--opt", default="zero", choices=["zero", "torch", "none"],
+                    help="none: forward + backward only (the compute the optimizer's exposed time is measured against)")
     ap.add_argument("--stage", type=int, default=1)
     args = ap.parse_args()
     torch.manual_seed(0)
@@ -84,6 +87,10 @@ def main():
 
         def opt_step():
             opt.step()
+    elif args.opt == "none":
+        def opt_step():
+            for p in model.parameters():
+                p.grad = None
     else:
         params = [p for p in model.parameters()]
         masters = [p.detach().float().clone().requires_grad_(True) for p in params]
