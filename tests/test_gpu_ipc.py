@@ -130,7 +130,7 @@ def run_workers(target, world, pre=(), post=(), timeout=300):
 
 @pytest.mark.parametrize("world,stage,dt,mode", [(2, 1, "bf16", "R16"), (2, 2, "fp16", "R16"), (2, 3, "bf16", "R16"),
                                                  (2, 0, "bf16", "R16"), (3, 2, "bf16", "R32"),
-                                                 (4, 3, "fp16", "R16")])
+                                                 (4, 3, "fp16", "R16"), (8, 2, "bf16", "R16"), (8, 3, "fp16", "R32")])
 def test_processes_share_one_gpu(world, stage, dt, mode):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
