@@ -522,6 +522,7 @@ def main():
     eng, cfg, grad_buf, grads = build(args.dtype)
     info = eng.info
     nb = info.n_buckets
+    info_buckets = list(eng.buckets)
     res = timed(eng, args.steps)
     rec = res["rec"]
     assert rec.overflow == 0 and rec.t >= args.steps, "benchmark steps must not be skipped"
@@ -576,6 +577,17 @@ def main():
                                     "all_reduce": res["sent"][2], "total": counted},
             "closed_form": closed, "closed_form_name": "3 Psi'(N-1)/N" if args.stage == 3 else "2 Psi'(N-1)/N",
             "equal": counted == closed}
+    if args.stage == 3 and N > 1:
+        # the paper's 3 Psi gathers every layer in the forward and again in the backward;
+        # the gather pool still holds the last prefetch_depth + 1 layers of the forward when the
+        # backward starts, and those are reused, not gathered again
+        sizes = {}
+        for b in info_buckets:
+            sizes[b.layer] = sizes.get(b.layer, 0) + b.size
+        reused = sum(sizes[L] for L in sorted(sizes)[-(cfg.prefetch_depth + 1):])
+        expected = closed - reused // N * (N - 1)
+        comm.update({"turnaround_reuse_elems": reused, "expected_with_reuse": expected,
+                     "equal": counted == expected, "within_closed_form": counted <= closed})
     if N > 1:
         # bus bandwidth in the nccl-tests convention, (S / t) (N-1)/N with S = the 16-bit buffer
         # (2 Psi' bytes); the phases overlap HBM work (the flattens; the Adam of the fused AG)
