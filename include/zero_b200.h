@@ -304,8 +304,10 @@ zero_status zero_reduce_grads(struct zero_ctx* ctx, uint32_t bucket, const void*
  * the all-gather buffer, then the all-gather (stages 1/2, "all-gather ... at
  * the end of each training step"; stage 0 updates everything locally; stage 3
  * keeps only the shard).  host_out (optional, pinned host memory for
- * asynchrony) receives the step record when the step's work completes (read it
- * after synchronizing the compute stream).  An overflow skips the update on the
+ * asynchrony) receives the step record by the time the step's work completes (read it
+ * after synchronizing the compute stream): UVA-mapped pinned memory (cudaHostAlloc /
+ * torch pin_memory) is written directly by the decision kernel, other memory by a D2H
+ * copy at the end of the step.  An overflow skips the update on the
  * device (t, m, v, master unchanged; the loss scale is halved when dynamic); the host
  * never waits.  The caller's compute stream is ordered after the step; with the
  * cross-process PEER transport the step ends with a device barrier, so every
