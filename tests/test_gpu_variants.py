@@ -78,3 +78,35 @@ def test_small_bucket_batching_permuted_order(monkeypatch):
         p.compare_info(oi, gi)
     p.compare()
     p.destroy()
+
+
+@pytest.mark.parametrize("n", [1, 4])
+def test_step_record_pinned_and_pageable(n):
+    """zero_step's host_out: pinned (UVA-mapped) memory is written by the decision kernel, any
+    other host memory by a D2H copy at the end of the step; both equal ZERO_Q_STEP's record."""
+    import ctypes as C
+    from paper_1910_02054_b200.zero import CStepInfo, _check, lib
+    ts = synth.mlp_layout((300, 200, 100))
+    p = Pair(Run(ts, n, 2, OS.AdamConfig.defaults("fp16", max_grad_norm=1e-2), cap=1 << 13, inject=(1,)))
+    for s in range(3):
+        host = [p.grads(r, s) for r in range(n)]
+        dev = [[g.cuda() for g in h] for h in host]
+        for k in reversed(range(len(p.lay.buckets))):
+            for r in range(n):
+                p.engines[r].reduce_grads(k, dev[r])
+        pageable = [CStepInfo() for _ in range(n)]
+        for r in range(n):
+            e = p.engines[r]
+            ptr = C.pointer(pageable[r]) if r % 2 == 0 else e._info_ptr
+            _check(lib.zero_step(e._ctx, ptr), e._ctx)
+        torch.cuda.synchronize()
+        OS.step(p.ost, [OS.grads_from_torch(h) for h in host], p.run.cfg)
+        for r in range(n):
+            e = p.engines[r]
+            ref = e.step_info()
+            got = pageable[r] if r % 2 == 0 else C.cast(e._info_ptr, C.POINTER(CStepInfo)).contents
+            assert (got.t, got.overflow, got.loss_scale, got.clip, got.grad_norm) == \
+                   (ref.t, ref.overflow, ref.loss_scale, ref.clip, ref.grad_norm), (s, r)
+            assert got.overflow == (s == 1)
+    p.compare()
+    p.destroy()
