@@ -212,8 +212,8 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
  *  gred    reduced-gradient shard: stages 2/3 R16 2*Psi'/N_d, R32 4*Psi'/N_d;
  *          stage 1 R32 4*Psi'/N_d; 0 otherwise
  *  gather  stage 3, NCCL/PEER: (prefetch_depth + 1) * max layer elements * 2
- *  scratch device state, norm slots, partial sums, segment table, signals (< 1 MB;
- *          at N_d == 1 plus 14 KB of per-CTA norm partials per bucket launch)
+ *  scratch device state, norm slots, partial sums, segment table, signals (< 1 MB),
+ *          plus 14 KB of per-CTA epilogue partials per bucket slot (e.g. 1.7 MB at 7.5B)
  * The grad/gred/gather/scratch arenas are the only transient buffers: nothing is
  * allocated during a step (M_D). */
 typedef struct {
