@@ -643,7 +643,8 @@ def main():
     # pinned memory + the step + D2H of the step record, every step
     if not args.no_e2e:
         try:
-            line["e2e"] = run_e2e(args, eng, grad_buf, grads, tensors, stream, dev, psi_total, ms, barrier)
+            line["e2e"] = run_e2e(args, eng, make_step(eng), grad_buf, grads, tensors, stream, dev, psi_total, ms,
+                                  barrier)
         except RuntimeError as exc:     # e.g. pinned host memory exhausted by N ranks
             line["e2e"] = {"value": None, "unit": "Gparams/s", "note": f"not measured: {exc}"}
             barrier()
@@ -686,13 +687,12 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(args, eng, grad_buf, grads, tensors, stream, dev, psi_total, ms, barrier):
+def run_e2e(args, eng, one_step, grad_buf, grads, tensors, stream, dev, psi_total, ms, barrier):
     """Every step copies that step's gradients H2D from pinned host memory and reads the
     step record D2H.  The copy of step s+1 (copy stream, second device buffer) overlaps
     step s; the host reads step s's record before issuing step s+2."""
     import torch
     import synth
-    nb = eng.info.n_buckets
     host = torch.empty(grad_buf.numel(), dtype=grad_buf.dtype, pin_memory=True)
     host.copy_(grad_buf)
     bufs = [grad_buf, torch.empty_like(grad_buf)]
@@ -712,8 +712,6 @@ def run_e2e(args, eng, grad_buf, grads, tensors, stream, dev, psi_total, ms, bar
     h2d_ms = h0.elapsed_time(h1)
     barrier()
     K = args.e2e_steps
-    layer_ids = sorted({b.layer for b in eng.buckets})
-    layer_buckets = {L: [k for k, b in enumerate(eng.buckets) if b.layer == L] for L in layer_ids}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
     e0.record(copy_stream)
@@ -724,19 +722,7 @@ def run_e2e(args, eng, grad_buf, grads, tensors, stream, dev, psi_total, ms, bar
         cur = s % 2
         stream.wait_event(copied[cur])
         eng.set_grads(views[cur])
-        if args.stage == 3:
-            for L in layer_ids:
-                eng.gather_params(L)
-                eng.release_params(L)
-            for L in reversed(layer_ids):
-                eng.gather_params(L)
-                for k in reversed(layer_buckets[L]):
-                    eng.reduce_grads(k)
-                eng.release_params(L)
-        else:
-            for k in reversed(range(nb)):
-                eng.reduce_grads(k)
-        eng.step()                              # + 32-byte step record D2H into pinned memory
+        one_step()                              # the whole step; its 32-byte record lands in pinned memory
         consumed[cur].record(stream)            # joined: the flattens have read bufs[cur]
         if s + 1 < K:
             nxt = (s + 1) % 2
