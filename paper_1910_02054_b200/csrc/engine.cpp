@@ -202,6 +202,7 @@ struct zero_ctx {
   bool rs_cta_partials = true;                     // ZERO_RS_CTA_PARTIALS=0: last-CTA combine in each reduce-scatter
   int rs_ctas = 4, rs_u = 0;                       // ZERO_RS_CTAS (CTAs per SM), ZERO_RS_U (0 = per-N default)
   int rs_pipe = 1;                                 // ZERO_RS_PIPE: 1 = software-pipelined pull (default), 0 = plain
+  bool rs_multi = true;                            // ZERO_RS_MULTI=0: simulated ranks' pulls launched per rank
   // ZeRO x MP (R-MP1): per-slot norm weights (0 for MP-replicated buckets on MP rank > 0)
   double* slot_w = nullptr;
   std::vector<double> slot_w_host;
@@ -788,6 +789,7 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   if (const char* ev = getenv("ZERO_RS_CTAS")) c->rs_ctas = std::max(1, std::min(8, atoi(ev)));
   if (const char* ev = getenv("ZERO_RS_U")) c->rs_u = atoi(ev);
   if (const char* ev = getenv("ZERO_RS_PIPE")) c->rs_pipe = atoi(ev);
+  if (const char* ev = getenv("ZERO_RS_MULTI")) c->rs_multi = atoi(ev) != 0;
   if (const char* ev = getenv("ZERO_SMALL_BUCKET")) c->small_bucket = strtoull(ev, nullptr, 10);
   if (const char* ev = getenv("ZERO_FLAT_STREAMS"))
     c->n_flat_streams = std::max(1, std::min(zero_ctx::kMaxFlatStreams, atoi(ev)));
@@ -1171,8 +1173,7 @@ zero_status issue_pull_rs_all(ZeroGroup* g, uint32_t k) {
   int grid = 0;
   for (int j = 0; j < g->n; ++j) grid = fill_pull_rs(g->ranks[j], g, k, m.r[j]);
   zero_ctx* c = g->ranks[0];
-  static const bool multi = !getenv("ZERO_RS_MULTI") || atoi(getenv("ZERO_RS_MULTI")) != 0;
-  const cudaError_t e = multi ? launch_reduce_scatter_multi(m, grid, c->comm_stream) : cudaErrorNotSupported;
+  const cudaError_t e = c->rs_multi ? launch_reduce_scatter_multi(m, grid, c->comm_stream) : cudaErrorNotSupported;
   if (e == cudaSuccess) {
     c->launches++;
   } else if (e == cudaErrorNotSupported) {

@@ -65,3 +65,39 @@ def test_random_configuration(seed):
                                    torch.from_numpy(p.ost.p16[t].view("int16")))
             e.release_params(L)
     p.destroy()
+
+
+KNOBS = {
+    "ZERO_RS_PIPE": ["0", "1", "2", "3"],
+    "ZERO_RS_CTA_PARTIALS": ["0", "1"],
+    "ZERO_RS_MULTI": ["0", "1"],
+    "ZERO_RS_CTAS": ["2", "4", "6"],
+    "ZERO_SMALL_BUCKET": ["0", "64", str(1 << 20)],
+    "ZERO_ADAM_VARIANT": [None, "0", "1", "21"],
+    "ZERO_FLAT_STREAMS": ["1", "2", "3"],
+    "ZERO_FLAT_CTA_PARTIALS": ["0", "1"],
+}
+
+
+@pytest.mark.parametrize("seed", range(1000, 1060))
+def test_random_configuration_and_launch_knobs(monkeypatch, seed):
+    """As above, with every launch knob drawn at random too (each one selects another kernel
+    body, grid or batching path) and the buckets reduced in a random order each step."""
+    rnd = random.Random(seed * 7 + 1)
+    for k, choices in KNOBS.items():
+        v = rnd.choice(choices)
+        if v is None:
+            monkeypatch.delenv(k, raising=False)
+        else:
+            monkeypatch.setenv(k, v)
+    ts, n, a, cap, stage, cfg, pool, depth = _case(seed)
+    run = Run(ts, n, stage, cfg, align=a, cap=cap, inject=(1,) if seed % 4 == 0 else (), pool=pool, prefetch=depth)
+    p = Pair(run)
+    nb = len(p.lay.buckets)
+    for s in range(3):
+        order = list(range(nb))
+        rnd.shuffle(order)
+        oi, gi = p.step(bucket_order=order)
+        p.compare_info(oi, gi)
+    p.compare()
+    p.destroy()
