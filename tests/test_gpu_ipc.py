@@ -369,3 +369,95 @@ def _gather_overlap_worker(rank, world, port, q, distinct=False):
 def test_stage3_gathers_overlap_compute():
     msgs = run_workers(_gather_overlap_worker, 2)
     assert msgs == ["ok", "ok"], msgs
+
+
+def _soak_worker(rank, world, port, stage, dt, mode, steps, q):
+    """Many steps over the CUDA-IPC peer table with NO host synchronization between them (the
+    ranks race ahead through the device-side epoch signals), random bucket orders and a few
+    injected overflows; the state after the last step must equal the oracle bit for bit."""
+    import random
+    import sys
+    import traceback
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "tests")]
+    try:
+        import numpy as np
+        import torch.distributed as dist
+        import synth
+        from harness import bits16, bits32, zcfg_from_oracle
+        from oracle import layout as OL
+        from oracle import step as OS
+        from paper_1910_02054_b200 import ZeroEngine
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        ts = synth.mlp_layout((120, 90, 60, 30))
+        nl, ll = [t.numel for t in ts], [t.layer for t in ts]
+        cfg = OS.AdamConfig.defaults(dt, reduce_mode=mode, max_grad_norm=0.05)
+        cap = 1 << 11
+        e = ZeroEngine(nl, ll, world, rank, stage, zcfg_from_oracle(cfg), "peer", align=64, bucket_cap=cap)
+        e.link_peers()
+        masters = synth.master_values(ts, 1)
+        e.load_master([torch.from_numpy(a).cuda() for a in masters])
+        ost = OS.init_state(masters, cfg)
+        lay = OL.make_layout(nl, ll, world, 64, cap)
+        inject = {steps // 3, (2 * steps) // 3}
+        # every step's gradients of every rank, generated up front (the oracle's loss scale path
+        # is replayed first so that fp16 gradients are drawn at the scale each step sees)
+        host_all = []
+        for s in range(steps):
+            scale = ost.S if dt == "fp16" else 1.0
+            host = [synth.grads16(ts, 1, r, s, dt, scale=scale) for r in range(world)]
+            if s in inject:
+                host[1][0] = host[1][0].clone()
+                host[1][0][3] = float("inf")
+            OS.step(ost, [OS.grads_from_torch(h) for h in host], cfg)
+            host_all.append(host[rank])
+        dev_all = [[g.cuda() for g in h] for h in host_all]
+        torch.cuda.synchronize()
+        dist.barrier()
+        order_rng = random.Random(7)      # the same bucket order on every rank
+        layers = sorted({b.layer for b in lay.buckets})
+        for s in range(steps):
+            order = list(range(e.info.n_buckets))
+            order_rng.shuffle(order)
+            if stage == 3:                # forward gathers (prefetch) interleaved with the step
+                for L in layers:
+                    e.gather_params(L)
+                    e.release_params(L)
+            for k in order:
+                e.reduce_grads(k, dev_all[s])
+            e.step()
+        info = e.step_info()              # the only synchronization
+        assert info.t == ost.t, (info.t, ost.t)
+        spans = {p.tensor: b.base + p.bucket_off for b in lay.buckets for p in b.pieces if p.tensor_off == 0}
+
+        def flat(arrs, dtype):
+            out = np.zeros(lay.psi_padded, dtype)
+            for t, a in enumerate(arrs):
+                out[spans[t]:spans[t] + a.size] = a
+            return out
+
+        P32, M, V = e.shard()
+        for name, gpu, ref in (("p32", P32, ost.p32), ("m", M, ost.m), ("v", V, ost.v)):
+            rf = flat(ref, np.float32)
+            want = rf if stage == 0 else np.concatenate(
+                [rf[lo:hi] for lo, hi in (lay.owned_range(k, rank) for k in range(len(lay.buckets)))])
+            assert np.array_equal(bits32(gpu), want.view(np.uint32)), name
+        if stage in (1, 2):
+            assert np.array_equal(bits16(e.p16_arena()), flat(ost.p16, np.uint16)), "replica"
+        torch.cuda.synchronize()
+        dist.barrier()
+        e.destroy()
+        dist.destroy_process_group()
+        q.put("ok")
+    except Exception:
+        q.put(traceback.format_exc())
+        raise
+
+
+@pytest.mark.parametrize("world,stage,dt,mode", [(2, 2, "bf16", "R16"), (3, 1, "fp16", "R32"), (4, 3, "bf16", "R16"),
+                                                 (2, 0, "fp16", "R16")])
+def test_soak_no_host_sync(world, stage, dt, mode):
+    msgs = run_workers(_soak_worker, world, pre=(stage, dt, mode, 120), timeout=600)
+    assert msgs == ["ok"] * world, msgs
