@@ -242,6 +242,9 @@ struct zero_ctx {
   int pend_lo = -1, pend_hi = -1;
   std::vector<std::pair<uint32_t, FlatPiece>> pend_pieces;  // (bucket, piece with its source resolved)
   uint64_t small_bucket = 1ull << 20;              // ZERO_SMALL_BUCKET (elements; 0 = never batch)
+  bool step_small = true;                          // ZERO_STEP_SMALL=0: no one-launch step for small models
+  bool fused_pending = false;                      // this zero_step runs as one cooperative launch
+  int step_small_grid = -1;                        // co-resident grid limit of that kernel (-1: not queried)
 
   // per-step tracking
   std::vector<uint8_t> reduced;
@@ -791,6 +794,7 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   if (const char* ev = getenv("ZERO_RS_PIPE")) c->rs_pipe = atoi(ev);
   if (const char* ev = getenv("ZERO_RS_MULTI")) c->rs_multi = atoi(ev) != 0;
   if (const char* ev = getenv("ZERO_SMALL_BUCKET")) c->small_bucket = strtoull(ev, nullptr, 10);
+  if (const char* ev = getenv("ZERO_STEP_SMALL")) c->step_small = atoi(ev) != 0;
   if (const char* ev = getenv("ZERO_FLAT_STREAMS"))
     c->n_flat_streams = std::max(1, std::min(zero_ctx::kMaxFlatStreams, atoi(ev)));
   if (const char* ev = getenv("ZERO_FLAT_PDL")) c->flat_pdl = atoi(ev) != 0 && c->transport == ZERO_TRANSPORT_LOCAL;
@@ -1070,41 +1074,49 @@ bool batchable(const zero_ctx* c, uint32_t k) {
 // one launch for the pending run of adjacent small buckets [pend_lo, pend_hi] (N_d = 1): their
 // pieces tile [base_lo, base_hi + B_hi) contiguously; the epilogue partials go to the first
 // bucket's slot and the run's other slots are cleared
-zero_status flush_small(zero_ctx* c, bool on_caller_stream = false, bool* decided = nullptr, void* rec_dev = nullptr) {
-  if (c->pend_lo < 0) return ZERO_OK;
+// the pending run's flatten arguments (pieces in bucket order, relative to the run's first
+// bucket); returns the run's element count.  per_cta is left to the caller (grid-dependent)
+uint64_t pending_flat_args(zero_ctx* c, FlatArgs& a) {
   std::stable_sort(c->pend_pieces.begin(), c->pend_pieces.end(),
                    [](const std::pair<uint32_t, FlatPiece>& x, const std::pair<uint32_t, FlatPiece>& y) {
                      return x.first < y.first;
                    });
   const uint32_t lo = (uint32_t)c->pend_lo, hi = (uint32_t)c->pend_hi;
   const uint64_t base_lo = c->buckets[lo].base;
-  FlatArgs a{};
+  a = FlatArgs{};
   a.n_pieces = (int)c->pend_pieces.size();
   for (int j = 0; j < a.n_pieces; ++j) {
     FlatPiece fp = c->pend_pieces[j].second;
     fp.dst_off += c->buckets[c->pend_pieces[j].first].base - base_lo;
     a.pieces[j] = fp;
   }
-  const uint64_t total = c->buckets[hi].base + c->buckets[hi].size - base_lo;
-  cudaStream_t fs = c->stream;
-  GridPartials* fpart = c->part_compute;
-  if (!on_caller_stream)
-    if (zero_status s = pick_flat_stream(c, &fs, &fpart)) return s;
-  const int grid = grid_for((total + 2047) / 2048, c->flat_ctas, c->sms);
   const int slot = c->slot_base[lo];
-  a.per_cta = align_up((total + grid - 1) / grid, 8);
   a.src_dtype = c->gdt;
   a.dst_dtype = c->pdt;
   a.epilogue = 1;
   a.dst = c->flat_dst(lo);
   a.sigma = c->cfg.grad_prescale;
   a.st = c->st;
-  a.part = fpart;
   a.slot = c->slots + slot;
   a.cta_sum = c->cta_sum + (size_t)slot * kMaxGrid;
   a.cta_flag = c->cta_flag + (size_t)slot * kMaxGrid;
   a.cta_grid = c->cta_grid + slot;
   a.clear_slots = (uint32_t)(c->slot_base[hi] - slot);   // one slot per batchable bucket
+  return c->buckets[hi].base + c->buckets[hi].size - base_lo;
+}
+
+zero_status flush_small(zero_ctx* c, bool on_caller_stream = false, bool* decided = nullptr, void* rec_dev = nullptr) {
+  if (c->pend_lo < 0) return ZERO_OK;
+  const uint32_t lo = (uint32_t)c->pend_lo, hi = (uint32_t)c->pend_hi;
+  FlatArgs a;
+  const uint64_t total = pending_flat_args(c, a);
+  cudaStream_t fs = c->stream;
+  GridPartials* fpart = c->part_compute;
+  if (!on_caller_stream)
+    if (zero_status s = pick_flat_stream(c, &fs, &fpart)) return s;
+  const int grid = grid_for((total + 2047) / 2048, c->flat_ctas, c->sms);
+  a.per_cta = align_up((total + grid - 1) / grid, 8);
+  a.part = fpart;
   // the whole step in this launch (zero_step, a small model): its last CTA also decides
   if (decided && lo == 0 && hi + 1 == c->info.n_buckets && c->n_slots == (int)c->info.n_buckets) {
     a.decide_st = c->st;
@@ -1119,6 +1131,62 @@ zero_status flush_small(zero_ctx* c, bool on_caller_stream = false, bool* decide
   c->pend_lo = c->pend_hi = -1;
   c->pend_pieces.clear();
   return ZERO_OK;
+}
+
+// N_d = 1, a small model whose every bucket is in the pending run: the whole step can be one
+// cooperative launch (flatten + epilogue, decision, Adam), unless a variant is forced, the
+// stream is being captured, or the kernel's co-resident grid is too small
+int step_small_grid(zero_ctx* c, StepSmallArgs* out, void* rec_dev);
+
+bool fused_step_ok(zero_ctx* c) {
+  if (c->transport != ZERO_TRANSPORT_LOCAL || !c->step_small || c->adam_variant_env) return false;
+  if (c->pend_lo != 0 || c->pend_hi + 1 != (int)c->info.n_buckets || c->n_slots != (int)c->info.n_buckets) return false;
+  if (c->S_e > c->adam_small) return false;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(c->stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return false;
+  }
+  return step_small_grid(c, nullptr, nullptr) > 0;
+}
+
+// the fused step's arguments and grid (0: not launchable)
+int step_small_grid(zero_ctx* c, StepSmallArgs* out, void* rec_dev) {
+  StepSmallArgs a{};
+  const uint64_t total = pending_flat_args(c, a.f);
+  a.f.decide_part = c->part_comm;            // the grid barrier's words
+  AdamArgs& d = a.adam;
+  d.p32 = c->p32;
+  d.m = c->m;
+  d.v = c->v;
+  d.G = (c->stage <= 1) ? (const void*)c->grad : (const void*)c->gred;
+  d.g_dtype = c->pdt;
+  d.p_dtype = c->pdt;
+  d.n_p16 = 1;
+  d.p16[0] = c->p16;
+  d.segs = c->segs;
+  d.n_segs = (int)c->segs_host.size();
+  d.total = c->S_e;
+  d.beta1 = c->cfg.beta1;
+  d.beta2 = c->cfg.beta2;
+  d.eps = c->cfg.eps;
+  d.omb1 = 1.0f - c->cfg.beta1;
+  d.omb2 = 1.0f - c->cfg.beta2;
+  d.wd = c->cfg.weight_decay > 0.0f ? 1 : 0;
+  d.lrwd = (float)((double)c->cfg.lr * (double)c->cfg.weight_decay);
+  d.st = c->st;
+  a.dp = decide_params(c);
+  a.dp.rec_out = rec_dev;
+  a.st = c->st;
+  a.out = c->my_partial;
+  if (c->step_small_grid < 0) c->step_small_grid = step_small_max_grid(a);
+  const uint64_t want = std::max<uint64_t>(std::max<uint64_t>((total + 2047) / 2048, (c->S_e + 2047) / 2048), 1);
+  const int grid = (int)std::min<uint64_t>(want, (uint64_t)std::min(c->step_small_grid, kMaxGrid));
+  if (grid <= 0) return 0;
+  a.f.per_cta = align_up((total + grid - 1) / grid, 8);
+  d.per_cta = align_up((c->S_e + grid - 1) / grid, 8);
+  if (out) *out = a;
+  return grid;
 }
 
 // LOCAL, small bucket k: join (or start) the pending run; the sources are resolved now
@@ -1466,8 +1534,14 @@ zero_status step_inputs(zero_ctx* c, PartialPtrs& pp, zero_ctx::StepEvents*& ev,
                    c->info.n_buckets);
   }
 
-  // the pending run of small buckets (N_d = 1), on the caller's stream: the step follows it there
-  if (zero_status s = flush_small(c, true, decided, rec_dev)) return s;
+  // the pending run of small buckets (N_d = 1), on the caller's stream: the step follows it there;
+  // when the run is the whole (small) model, the step becomes one cooperative launch instead
+  if (decided && fused_step_ok(c)) {
+    c->fused_pending = true;
+    *decided = true;
+  } else if (zero_status s = flush_small(c, true, decided, rec_dev)) {
+    return s;
+  }
   if (c->gather_stream) {  // no rank's Adam may rewrite a shard a gather still reads
     CK(cudaEventRecord(c->ev_gjoin, c->gather_stream));
     CK(cudaStreamWaitEvent(c->comm_stream, c->ev_gjoin, 0));
@@ -1523,16 +1597,29 @@ zero_status step_finish(zero_ctx* c, const PartialPtrs& pp, zero_ctx::StepEvents
                         bool decided = false) {
   ZeroGroup* g = c->group;
   void* rec_dev = mapped_record(c, host_out);
-  if (!decided) {
-    DecideParams p = decide_params(c);
-    p.rec_out = rec_dev;
-    CK(launch_decide_global(pp, c->st, p, c->comm_stream));
+  if (c->fused_pending) {   // flatten + decision + Adam in one cooperative launch (a small model)
+    StepSmallArgs a;
+    const int grid = step_small_grid(c, &a, rec_dev);
+    c->fused_pending = false;
+    c->pend_lo = c->pend_hi = -1;
+    c->pend_pieces.clear();
+    if (ev) CK(cudaEventRecord(ev->a0, c->comm_stream));
+    CK(launch_step_small(a, grid, c->comm_stream));
     c->launches++;
+    c->adam_launches++;
+    if (ev) CK(cudaEventRecord(ev->a1, c->comm_stream));
+  } else {
+    if (!decided) {
+      DecideParams p = decide_params(c);
+      p.rec_out = rec_dev;
+      CK(launch_decide_global(pp, c->st, p, c->comm_stream));
+      c->launches++;
+    }
+    if (ev) CK(cudaEventRecord(ev->a0, c->comm_stream));
+    zero_status s = issue_adam(c, g);
+    if (s != ZERO_OK) return s;
+    if (ev) CK(cudaEventRecord(ev->a1, c->comm_stream));
   }
-  if (ev) CK(cudaEventRecord(ev->a0, c->comm_stream));
-  zero_status s = issue_adam(c, g);
-  if (s != ZERO_OK) return s;
-  if (ev) CK(cudaEventRecord(ev->a1, c->comm_stream));
 
   if (c->transport == ZERO_TRANSPORT_NCCL && (c->stage == 1 || c->stage == 2)) {
     // all-gather the updated 16-bit parameters per bucket, in place

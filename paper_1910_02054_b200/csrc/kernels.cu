@@ -1582,10 +1582,11 @@ struct AdamIO {
 
 // MINB: CTAs per SM the register budget is sized for; U: 8-element groups per
 // thread per iteration (all loads of an iteration are issued before any math).
+template <int PDT, int GDT, int U>
+__device__ __forceinline__ void adam_body(const AdamArgs& a, const AdamScalars& c);
+
 template <int PDT, int GDT, int MINB, int U>
 __global__ void __launch_bounds__(kThreads, MINB) k_adam(const __grid_constant__ AdamArgs a) {
-  using P = H16<PDT>;
-  using IO = AdamIO<PDT, GDT>;
   if (a.st->skip) return;  // overflow: the whole step is skipped (reading c-4)
   AdamScalars c;
   c.inv = a.st->inv_adam;
@@ -1599,6 +1600,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_adam(const __grid_constant__
   c.omb2 = a.omb2;
   c.lrwd = a.lrwd;
   c.wd = a.wd;
+  adam_body<PDT, GDT, U>(a, c);
+}
+
+// the register-staged Adam over this CTA's contiguous range of the shard (k_adam and the
+// fused small-model step)
+template <int PDT, int GDT, int U>
+__device__ __forceinline__ void adam_body(const AdamArgs& a, const AdamScalars& c) {
+  using P = H16<PDT>;
+  using IO = AdamIO<PDT, GDT>;
   const uint64_t lo = (uint64_t)blockIdx.x * a.per_cta;
   if (lo >= a.total) return;
   const uint64_t hi = lo + a.per_cta < a.total ? lo + a.per_cta : a.total;
@@ -2032,6 +2042,125 @@ cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int variant
     if (a.g_dtype == DT_F32) return launch_adam_t<DT_BF16, DT_F32>(a, grid, s, variant);
   }
   return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------------------
+// N_d = 1, a small model (the whole step is a few microseconds of bandwidth): flatten +
+// epilogue, decision, fused Adam in ONE cooperative launch.  Phase A is k_flatten's body
+// over every bucket (per-CTA {sum, flag} partials); after a grid barrier CTA 0 combines the
+// partials in CTA order and makes the decision (decide_apply, as k_decide_*); after a
+// second barrier every CTA runs the register Adam body over its range, reading the scalars
+// the decision wrote (L1-bypassing loads: the line was cached before the barrier).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int g = *(volatile unsigned int*)gen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*(volatile unsigned int*)gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int SDT, int DDT, bool kCopy>
+__global__ void __launch_bounds__(kThreads, 4) k_step_small(const __grid_constant__ StepSmallArgs a) {
+  // barrier words: the DevState's record padding is not used; a GridPartials ticket pair is
+  GridPartials* bar = a.f.decide_part;
+  double sumsq = 0.0;
+  uint32_t flag = 0;
+  const float inv = a.f.st->inv_cur;
+  if (pow2_at_most_one(inv)) {
+    flatten_body<SDT, DDT, kCopy, 2, 2>(a.f, inv, sumsq, flag);
+    flag = isfinite(sumsq) ? 0u : 1u;
+    sumsq *= (double)inv * (double)inv;
+  } else {
+    flatten_body<SDT, DDT, kCopy, 2, 1>(a.f, inv, sumsq, flag);
+  }
+  block_reduce(sumsq, flag);
+  if (threadIdx.x == 0) {
+    a.f.cta_sum[blockIdx.x] = sumsq;
+    a.f.cta_flag[blockIdx.x] = flag;
+  }
+  grid_barrier(&bar->ticket, &bar->pad);
+  if (blockIdx.x == 0) {   // the decision, from the partials in CTA order
+    double s = 0.0;
+    uint32_t f = 0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+      s += __ldcg(&a.f.cta_sum[i]);
+      f |= __ldcg(&a.f.cta_flag[i]);
+    }
+    block_reduce(s, f);
+    if (threadIdx.x == 0) {
+      a.out->sumsq = s;
+      a.out->flag = f ? 1.0 : 0.0;
+      decide_apply(s, f ? 1.0 : 0.0, a.st, a.dp);
+      __threadfence();
+    }
+  }
+  grid_barrier(&bar->ticket, &bar->pad);
+  if (__ldcg(&a.st->skip)) return;   // overflow: the step is skipped (reading c-4)
+  AdamScalars c;
+  c.inv = __ldcg(&a.st->inv_adam);
+  c.step = __ldcg(&a.st->step_f);
+  c.rsb2 = __ldcg(&a.st->rsb2_f);
+  c.clip = __ldcg(&a.st->clip_f);
+  c.beta1 = a.adam.beta1;
+  c.beta2 = a.adam.beta2;
+  c.eps = a.adam.eps;
+  c.omb1 = a.adam.omb1;
+  c.omb2 = a.adam.omb2;
+  c.lrwd = a.adam.lrwd;
+  c.wd = a.adam.wd;
+  adam_body<DDT, DDT, 1>(a.adam, c);
+}
+
+template <int SD, int DD, bool CP>
+static cudaError_t step_small_t(const StepSmallArgs& a, int grid, cudaStream_t s, int* max_grid) {
+  if (max_grid) {
+    int per_sm = 0;
+    if (cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_small<SD, DD, CP>, kThreads, 0))
+      return e;
+    *max_grid = per_sm * sm_count();
+    return cudaSuccess;
+  }
+  void* args[] = {const_cast<StepSmallArgs*>(&a)};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_step_small<SD, DD, CP>), dim3(grid), dim3(kThreads),
+                                     args, 0, s);
+}
+
+static cudaError_t step_small_dispatch(const StepSmallArgs& a, int grid, cudaStream_t s, int* max_grid) {
+  const bool copy = a.f.sigma == 1.0f && a.f.src_dtype == a.f.dst_dtype;
+  if (a.adam.g_dtype != a.f.dst_dtype || a.adam.p_dtype != a.f.dst_dtype) return cudaErrorNotSupported;
+  if (a.f.dst_dtype == DT_F16) {
+    if (a.f.src_dtype == DT_F16) return copy ? step_small_t<DT_F16, DT_F16, true>(a, grid, s, max_grid)
+                                             : step_small_t<DT_F16, DT_F16, false>(a, grid, s, max_grid);
+    if (a.f.src_dtype == DT_F32) return step_small_t<DT_F32, DT_F16, false>(a, grid, s, max_grid);
+  } else if (a.f.dst_dtype == DT_BF16) {
+    if (a.f.src_dtype == DT_BF16) return copy ? step_small_t<DT_BF16, DT_BF16, true>(a, grid, s, max_grid)
+                                              : step_small_t<DT_BF16, DT_BF16, false>(a, grid, s, max_grid);
+    if (a.f.src_dtype == DT_F32) return step_small_t<DT_F32, DT_BF16, false>(a, grid, s, max_grid);
+  }
+  return cudaErrorNotSupported;
+}
+
+int step_small_max_grid(const StepSmallArgs& a) {
+  int g = 0;
+  if (step_small_dispatch(a, 0, nullptr, &g) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return g;
+}
+
+cudaError_t launch_step_small(const StepSmallArgs& a, int grid, cudaStream_t s) {
+  return step_small_dispatch(a, grid, s, nullptr);
 }
 
 // ---------------------------------------------------------------------------

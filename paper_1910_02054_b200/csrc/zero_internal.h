@@ -147,6 +147,16 @@ struct AdamArgs {
   const DevState* st;
 };
 
+// N_d = 1, a small model: the whole step -- flatten of every bucket with the overflow/norm
+// epilogue, the decision, the fused Adam -- as ONE cooperative launch (grid-wide barriers)
+struct StepSmallArgs {
+  FlatArgs f;                 // every bucket (one batched run); f.cta_sum/cta_flag: per-CTA partials
+  AdamArgs adam;              // per_cta for the same grid
+  DecideParams dp;
+  DevState* st;
+  RankPartial* out;
+};
+
 struct CopyArgs {             // multi-row 16-bit copy: pull all-gathers (a6/a7) and P_a's save/gather
   const void* src[kMaxRanks];
   void* dst[kMaxRanks];
@@ -229,6 +239,9 @@ cudaError_t launch_combine_partials(const PartialPtrs& pp, RankPartial* out, cud
 cudaError_t launch_decide_global(const PartialPtrs& partials, DevState* st, DecideParams p, cudaStream_t s);
 cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int variant);
 int adam_ctas_per_sm(int variant);
+// the largest co-resident grid of the fused small step (0: not available)
+int step_small_max_grid(const StepSmallArgs& a);
+cudaError_t launch_step_small(const StepSmallArgs& a, int grid, cudaStream_t s);
 bool adam_variant_is_tma(int variant);
 cudaError_t launch_copy(const CopyArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_load(const LoadArgs& a, cudaStream_t s);
