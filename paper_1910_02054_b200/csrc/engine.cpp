@@ -243,6 +243,7 @@ struct zero_ctx {
   std::vector<std::pair<uint32_t, FlatPiece>> pend_pieces;  // (bucket, piece with its source resolved)
   uint64_t small_bucket = 1ull << 20;              // ZERO_SMALL_BUCKET (elements; 0 = never batch)
   bool step_small = true;                          // ZERO_STEP_SMALL=0: no one-launch step for small models
+  int step_small_ctas = 0;                         // ZERO_STEP_SMALL_CTAS: grid cap of that launch (0 = occupancy)
   bool fused_pending = false;                      // this zero_step runs as one cooperative launch
   int step_small_grid = -1;                        // co-resident grid limit of that kernel (-1: not queried)
 
@@ -795,6 +796,7 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   if (const char* ev = getenv("ZERO_RS_MULTI")) c->rs_multi = atoi(ev) != 0;
   if (const char* ev = getenv("ZERO_SMALL_BUCKET")) c->small_bucket = strtoull(ev, nullptr, 10);
   if (const char* ev = getenv("ZERO_STEP_SMALL")) c->step_small = atoi(ev) != 0;
+  if (const char* ev = getenv("ZERO_STEP_SMALL_CTAS")) c->step_small_ctas = atoi(ev);
   if (const char* ev = getenv("ZERO_FLAT_STREAMS"))
     c->n_flat_streams = std::max(1, std::min(zero_ctx::kMaxFlatStreams, atoi(ev)));
   if (const char* ev = getenv("ZERO_FLAT_PDL")) c->flat_pdl = atoi(ev) != 0 && c->transport == ZERO_TRANSPORT_LOCAL;
@@ -1181,7 +1183,9 @@ int step_small_grid(zero_ctx* c, StepSmallArgs* out, void* rec_dev) {
   a.out = c->my_partial;
   if (c->step_small_grid < 0) c->step_small_grid = step_small_max_grid(a);
   const uint64_t want = std::max<uint64_t>(std::max<uint64_t>((total + 2047) / 2048, (c->S_e + 2047) / 2048), 1);
-  const int grid = (int)std::min<uint64_t>(want, (uint64_t)std::min(c->step_small_grid, kMaxGrid));
+  int cap = std::min(c->step_small_grid, kMaxGrid);
+  if (c->step_small_ctas > 0) cap = std::min(cap, c->step_small_ctas);
+  const int grid = (int)std::min<uint64_t>(want, (uint64_t)cap);
   if (grid <= 0) return 0;
   a.f.per_cta = align_up((total + grid - 1) / grid, 8);
   d.per_cta = align_up((c->S_e + grid - 1) / grid, 8);
