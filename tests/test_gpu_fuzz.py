@@ -76,6 +76,7 @@ KNOBS = {
     "ZERO_ADAM_VARIANT": [None, "0", "1", "21"],
     "ZERO_FLAT_STREAMS": ["1", "2", "3"],
     "ZERO_FLAT_CTA_PARTIALS": ["0", "1"],
+    "ZERO_STEP_SMALL": ["0", "1"],
 }
 
 

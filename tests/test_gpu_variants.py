@@ -7,7 +7,8 @@ held to the same bit-exact parity against the oracle as the defaults (test_gpu_p
 * the flatten without the batching of adjacent small buckets (ZERO_SMALL_BUCKET=0);
 * the reduce-scatter with a last-CTA combine instead of per-CTA partials, the plain
   (not software-pipelined) pull with other loads-in-flight settings, 256-bit loads;
-* the flatten's last-CTA combine (ZERO_FLAT_CTA_PARTIALS=0).
+* the flatten's last-CTA combine (ZERO_FLAT_CTA_PARTIALS=0);
+* a small model's whole step as one cooperative launch (ZERO_STEP_SMALL=1; N_d = 1).
 The knobs are environment variables read when the arenas are bound."""
 import pytest
 import torch
@@ -30,6 +31,7 @@ VARIANTS = {
     "rs_w16": {"ZERO_RS_PIPE": "2"},
     "rs_w16_pipe": {"ZERO_RS_PIPE": "3", "ZERO_RS_CTAS": "2"},
     "flat_grid_combine": {"ZERO_FLAT_CTA_PARTIALS": "0", "ZERO_SMALL_BUCKET": "0"},
+    "step_small_fused": {"ZERO_STEP_SMALL": "1"},
 }
 
 
