@@ -371,7 +371,7 @@ def test_stage3_gathers_overlap_compute():
     assert msgs == ["ok", "ok"], msgs
 
 
-def _soak_worker(rank, world, port, stage, dt, mode, steps, q):
+def _soak_worker(rank, world, port, stage, dt, mode, steps, q, distinct=False):
     """Many steps over the CUDA-IPC peer table with NO host synchronization between them (the
     ranks race ahead through the device-side epoch signals), random bucket orders and a few
     injected overflows; the state after the last step must equal the oracle bit for bit."""
@@ -390,7 +390,7 @@ def _soak_worker(rank, world, port, stage, dt, mode, steps, q):
         from paper_1910_02054_b200 import ZeroEngine
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(rank if distinct else 0)
         ts = synth.mlp_layout((120, 90, 60, 30))
         nl, ll = [t.numel for t in ts], [t.layer for t in ts]
         cfg = OS.AdamConfig.defaults(dt, reduce_mode=mode, max_grad_norm=0.05)

@@ -216,3 +216,11 @@ def test_stage3_gathers_overlap_compute_one_gpu_per_rank():
     from test_gpu_ipc import _gather_overlap_worker
     msgs = run_workers(_gather_overlap_worker, 2, post=(True,))
     assert msgs == ["ok", "ok"], msgs
+
+
+@pytest.mark.parametrize("world", WORLDS)
+@pytest.mark.parametrize("stage,dt,mode", [(2, "bf16", "R16"), (3, "fp16", "R32"), (1, "bf16", "R32")])
+def test_soak_no_host_sync_one_gpu_per_rank(world, stage, dt, mode):
+    from test_gpu_ipc import _soak_worker
+    msgs = run_workers(_soak_worker, world, pre=(stage, dt, mode, 200), post=(True,), timeout=900)
+    assert msgs == ["ok"] * world, msgs
