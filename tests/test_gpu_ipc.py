@@ -461,3 +461,85 @@ def _soak_worker(rank, world, port, stage, dt, mode, steps, q, distinct=False):
 def test_soak_no_host_sync(world, stage, dt, mode):
     msgs = run_workers(_soak_worker, world, pre=(stage, dt, mode, 120), timeout=600)
     assert msgs == ["ok"] * world, msgs
+
+
+def _scale_worker(rank, world, port, stage, steps, q, distinct=False):
+    """The c-9 invariant at scale over the product transport: every rank gets the same
+    gradients (GPT-2 1.5B layout, first 8 layer groups: 297M parameters, 2^26 buckets), so
+    the CUDA-IPC run must reproduce the N_d = 1 run bit for bit (the fp32 sum of N equal
+    16-bit values is exact, 1/N is a power of two).  Rank 0 runs the N_d = 1 reference too."""
+    import sys
+    import traceback
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "tests")]
+    try:
+        import torch.distributed as dist
+        import synth
+        from paper_1910_02054_b200 import ZeroConfig, ZeroEngine
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        dev = torch.device("cuda", rank if distinct else 0)
+        torch.cuda.set_device(dev)
+        ts = synth.CONFIGS["gpt2_1.5b_l8"]()
+        nl, ll = [t.numel for t in ts], [t.layer for t in ts]
+        zc = ZeroConfig.defaults("bf16")
+        e = ZeroEngine(nl, ll, world, rank, stage, zc, "peer", align=64, bucket_cap=1 << 26, device=dev)
+        e.link_peers()
+        one = ZeroEngine(nl, ll, 1, 0, stage, zc, "local", align=64, bucket_cap=1 << 26, device=dev) if rank == 0 else None
+        for i in range(len(ts)):
+            m = synth.gpu_masters(ts, 1, dev, only={i})
+            e.load_master(m)
+            if one:
+                one.load_master(m)
+        grads = [synth.gpu_grads_flat(ts, 1, 0, s, torch.bfloat16, dev)[1] for s in range(steps)]
+        torch.cuda.synchronize()
+        dist.barrier()
+        for s in range(steps):                     # no host synchronization between steps
+            for k in reversed(range(e.info.n_buckets)):
+                e.reduce_grads(k, grads[s])
+            e.step()
+            if one:
+                for k in reversed(range(one.info.n_buckets)):
+                    one.reduce_grads(k, grads[s])
+                one.step()
+        info = e.step_info()
+        assert info.t == steps and info.overflow == 0
+        # gather the ranks' shards (p32) and rank 0's replica to rank 0, compare with N_d = 1
+        P32 = e.shard()[0].cpu()
+        shards = [None] * world
+        dist.all_gather_object(shards, P32)
+        replica = e.p16_arena().cpu() if stage in (1, 2) else None
+        ok = True
+        if rank == 0:
+            p1 = one.shard()[0].cpu()
+            flat1 = {pc.tensor: b.base + pc.bucket_off for b in one.buckets
+                     for pc in one.pieces[b.first_piece:b.first_piece + b.n_pieces] if pc.tensor_off == 0}
+            flatn = {pc.tensor: b.base + pc.bucket_off for b in e.buckets
+                     for pc in e.pieces[b.first_piece:b.first_piece + b.n_pieces] if pc.tensor_off == 0}
+            full = torch.empty(e.info.psi_padded, dtype=torch.float32)
+            for b in e.buckets:
+                sl = b.size // world
+                for r in range(world):
+                    full[b.base + r * sl:b.base + (r + 1) * sl] = shards[r][b.shard_off:b.shard_off + sl]
+            for t, spec in enumerate(ts):
+                a, c = flat1[t], flatn[t]
+                ok = ok and torch.equal(p1[a:a + spec.numel].view(torch.int32), full[c:c + spec.numel].view(torch.int32))
+                if replica is not None:
+                    ok = ok and torch.equal(one.p16_arena().cpu()[a:a + spec.numel].view(torch.int16),
+                                            replica[c:c + spec.numel].view(torch.int16))
+        torch.cuda.synchronize()
+        dist.barrier()
+        e.destroy()
+        if one:
+            one.destroy()
+        dist.destroy_process_group()
+        q.put("ok" if ok else f"rank {rank}: differs from N_d = 1")
+    except Exception:
+        q.put(traceback.format_exc())
+        raise
+
+
+@pytest.mark.parametrize("world,stage", [(4, 2), (2, 1)])
+def test_ipc_replicated_gradients_at_scale(world, stage):
+    msgs = run_workers(_scale_worker, world, pre=(stage, 4), timeout=900)
+    assert msgs == ["ok"] * world, msgs
