@@ -224,3 +224,11 @@ def test_soak_no_host_sync_one_gpu_per_rank(world, stage, dt, mode):
     from test_gpu_ipc import _soak_worker
     msgs = run_workers(_soak_worker, world, pre=(stage, dt, mode, 200), post=(True,), timeout=900)
     assert msgs == ["ok"] * world, msgs
+
+
+@pytest.mark.parametrize("world", WORLDS)
+@pytest.mark.parametrize("stage", [1, 2])
+def test_ipc_replicated_gradients_at_scale_one_gpu_per_rank(world, stage):
+    from test_gpu_ipc import _scale_worker
+    msgs = run_workers(_scale_worker, world, pre=(stage, 4), post=(True,), timeout=900)
+    assert msgs == ["ok"] * world, msgs
