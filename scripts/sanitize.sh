@@ -8,7 +8,7 @@ cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out/sanitize
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 SEL="ragged or clipping or bucket_order or stage3_gather or (single_rank and bf16) or (config1_sim4 and bf16 and R16)"
-VAR="(variant_matches_oracle and (rs_plain_u2 or adam_tma or rs_grid_combine or rs_w16)) or batching"
+VAR="(variant_matches_oracle and (rs_plain_u2 or adam_tma or rs_grid_combine or rs_w16 or step_small)) or batching or step_record"
 PA="round_trip and (100003 or 197) or backward_layer_order or call_order"
 NC="r32_one_rank and bf16"
 for tool in memcheck racecheck synccheck initcheck; do
