@@ -130,6 +130,19 @@ def ncu_traffic(kernel: str):
         return None, None
 
 
+def min_over_ranks(value: int, device) -> int:
+    """Min of a per-rank integer over all ranks (identity without torch.distributed)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return value
+    if dist.get_backend() == "gloo":
+        device = torch.device("cpu")
+    t = torch.tensor([value], device=device, dtype=torch.int64)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return int(t.item())
+
+
 def max_over_ranks(value: float, device) -> float:
     """Max of a per-rank time over all ranks (identity without torch.distributed)."""
     import torch
@@ -642,12 +655,21 @@ def main():
     # e2e through the public API with HOST buffers: H2D of the step's gradients from
     # pinned memory + the step + D2H of the step record, every step
     if not args.no_e2e:
+        # the buffers first, then every rank agrees: a rank that cannot pin its host copy
+        # (e.g. host memory exhausted by N ranks) must not leave the others inside a step
         try:
-            line["e2e"] = run_e2e(args, eng, make_step(eng), grad_buf, grads, tensors, stream, dev, psi_total, ms,
-                                  barrier)
-        except RuntimeError as exc:     # e.g. pinned host memory exhausted by N ranks
-            line["e2e"] = {"value": None, "unit": "Gparams/s", "note": f"not measured: {exc}"}
-            barrier()
+            host = torch.empty(grad_buf.numel(), dtype=grad_buf.dtype, pin_memory=True)
+            spare = torch.empty_like(grad_buf)
+            ok, why = 1, None
+        except RuntimeError as exc:
+            host = spare = None
+            ok, why = 0, str(exc)
+        if min_over_ranks(ok, dev) == 1:
+            line["e2e"] = run_e2e(args, eng, make_step(eng), grad_buf, grads, host, spare, tensors, stream, dev,
+                                  psi_total, ms, barrier)
+        else:
+            line["e2e"] = {"value": None, "unit": "Gparams/s", "note": f"not measured: {why or 'a peer rank could not allocate its buffers'}"}
+        del host, spare
 
     # the same layout in fp16 with dynamic loss scaling (the paper's precision)
     if args.dtype == "bf16" and not args.no_fp16_key and not args.graph:
@@ -687,15 +709,14 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(args, eng, one_step, grad_buf, grads, tensors, stream, dev, psi_total, ms, barrier):
+def run_e2e(args, eng, one_step, grad_buf, grads, host, spare, tensors, stream, dev, psi_total, ms, barrier):
     """Every step copies that step's gradients H2D from pinned host memory and reads the
     step record D2H.  The copy of step s+1 (copy stream, second device buffer) overlaps
     step s; the host reads step s's record before issuing step s+2."""
     import torch
     import synth
-    host = torch.empty(grad_buf.numel(), dtype=grad_buf.dtype, pin_memory=True)
     host.copy_(grad_buf)
-    bufs = [grad_buf, torch.empty_like(grad_buf)]
+    bufs = [grad_buf, spare]
     views = [grads, [bufs[1][o:o + t.numel] for t, o in zip(tensors, synth.tensor_offsets(tensors))]]
     copy_stream = torch.cuda.Stream(dev)
     copied = [torch.cuda.Event(), torch.cuda.Event()]
@@ -737,7 +758,7 @@ def run_e2e(args, eng, one_step, grad_buf, grads, tensors, stream, dev, psi_tota
     e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / K, dev)
     e2e_dev_ms = max_over_ranks(e0.elapsed_time(e1) / K, dev)
     eng.set_grads(grads)
-    del host, bufs
+    del bufs
     nbytes = int(grad_buf.numel() * grad_buf.element_size())
     return {"value": psi_total / (e2e_ms * 1e-3) / 1e9, "unit": "Gparams/s",
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 32, "ms_per_step": e2e_ms, "steps": K,

@@ -186,3 +186,14 @@ def _max_over_ranks(rank, world):
 
 def test_bench_max_over_ranks():
     _run(2, "_max_over_ranks")
+
+
+def _min_over_ranks(rank, world):
+    import bench
+    assert bench.min_over_ranks(0 if rank == world - 1 else 1, torch.device("cpu")) == 0
+    assert bench.min_over_ranks(1, torch.device("cpu")) == 1
+
+
+def test_bench_min_over_ranks():
+    """bench.py's e2e leg runs only if every rank could allocate its buffers (MIN over ranks)."""
+    _run(2, "_min_over_ranks")
