@@ -694,9 +694,6 @@ zero_status zero_init(const zero_layout_desc* desc, int n_d, int rank, int stage
   const uint64_t P = c->info.psi_padded, S = c->info.shard;
   zero_sizes& z = c->sizes;
   c->opt_stride = align_up(c->S_e, 64);
-  // ZERO_OPT_PAD (elements, multiple of 64): extra distance between the master, m and v arrays
-  // (an experiment on DRAM channel balance; 0 by default)
-  if (const char* ev = getenv("ZERO_OPT_PAD")) c->opt_stride += align_up(strtoull(ev, nullptr, 10), 64);
   z.opt_bytes = 12ull * c->opt_stride;
   z.opt_stride_elems = c->opt_stride;
   z.p16_bytes = 2ull * (stage == 3 ? S : P);
