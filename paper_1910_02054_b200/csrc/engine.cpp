@@ -247,6 +247,8 @@ struct zero_ctx {
                                                    // grid barriers cost more than the launch they save)
   int step_small_ctas = 0;                         // ZERO_STEP_SMALL_CTAS: grid cap of that launch (0 = occupancy)
   bool fused_pending = false;                      // this zero_step runs as one cooperative launch
+  bool adam_pdl = false;                           // the Adam follows the whole-step flatten on its stream
+  bool adam_pdl_ok = true;                         // ZERO_ADAM_PDL=0: never launch the Adam with PDL
   int step_small_grid = -1;                        // co-resident grid limit of that kernel (-1: not queried)
 
   // per-step tracking
@@ -798,6 +800,7 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   if (const char* ev = getenv("ZERO_RS_MULTI")) c->rs_multi = atoi(ev) != 0;
   if (const char* ev = getenv("ZERO_SMALL_BUCKET")) c->small_bucket = strtoull(ev, nullptr, 10);
   if (const char* ev = getenv("ZERO_STEP_SMALL")) c->step_small = atoi(ev) != 0;
+  if (const char* ev = getenv("ZERO_ADAM_PDL")) c->adam_pdl_ok = atoi(ev) != 0;
   if (const char* ev = getenv("ZERO_STEP_SMALL_CTAS")) c->step_small_ctas = atoi(ev);
   if (const char* ev = getenv("ZERO_FLAT_STREAMS"))
     c->n_flat_streams = std::max(1, std::min(zero_ctx::kMaxFlatStreams, atoi(ev)));
@@ -1129,6 +1132,7 @@ zero_status flush_small(zero_ctx* c, bool on_caller_stream = false, bool* decide
     a.decide = decide_params(c);
     a.decide.rec_out = rec_dev;
     *decided = true;
+    c->adam_pdl = on_caller_stream && c->adam_pdl_ok;   // the Adam comes next on this stream
   }
   CK(launch_flatten(a, grid, fs, c->flat_vecs));
   c->launches++;
@@ -1478,6 +1482,8 @@ zero_status issue_adam(zero_ctx* c, ZeroGroup* g) {
   // register-staged kernel with 4 CTAs per SM is used (unless a variant is forced)
   if (!c->adam_variant_env && c->S_e <= c->adam_small) variant = 1;
   if (adam_variant_is_tma(variant) && !c->segs_aligned8) variant = 0;  // bulk copies need 16-B granules
+  a.pdl = (c->adam_pdl && variant == 1) ? 1 : 0;   // launch while the whole-step flatten finishes
+  c->adam_pdl = false;
   const int grid = grid_for((c->S_e + 2047) / 2048, adam_ctas_per_sm(variant), c->sms);
   a.per_cta = align_up((c->S_e + grid - 1) / grid, 8);
   a.beta1 = c->cfg.beta1;

@@ -1495,7 +1495,8 @@ __device__ void decide_apply(double sum, double flags, DevState* st, const Decid
     r[1] = (uint64_t)(overflow ? 1u : 0u) | ((uint64_t)__float_as_uint(S_used) << 32);
     r[2] = (uint64_t)__float_as_uint(clip);
     r[3] = (uint64_t)__double_as_longlong(norm);
-    __threadfence_system();
+    // no system fence: the caller reads the record after synchronizing the stream, and a
+    // kernel's writes are visible to the host once it has completed
   }
 }
 
@@ -1587,6 +1588,9 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a, const AdamScalars& 
 
 template <int PDT, int GDT, int MINB, int U>
 __global__ void __launch_bounds__(kThreads, MINB) k_adam(const __grid_constant__ AdamArgs a) {
+  // PDL (a.pdl): launched while the whole-step flatten that made the decision finishes; wait
+  // for it to complete (its writes visible) before reading the decision (a no-op otherwise)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (a.st->skip) return;  // overflow: the whole step is skipped (reading c-4)
   AdamScalars c;
   c.inv = a.st->inv_adam;
@@ -2027,7 +2031,21 @@ cudaError_t launch_adam_t(const AdamArgs& a, int grid, cudaStream_t s, int varia
   switch (variant) {
     case 11: return launch_adam_tma_t<PD, GD, 4096, 2>(a, grid, s);
     case 21: return launch_adam_tma_st_t<PD, GD, 4096, 2>(a, grid, s);
-    case 1: k_adam<PD, GD, 4, 1><<<grid, kThreads, 0, s>>>(a); break;
+    case 1:
+      if (a.pdl) {   // a programmatic dependent of the flatten before it on this stream
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kThreads);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, k_adam<PD, GD, 4, 1>, a);
+      }
+      k_adam<PD, GD, 4, 1><<<grid, kThreads, 0, s>>>(a);
+      break;
     default: k_adam<PD, GD, 2, 1><<<grid, kThreads, 0, s>>>(a); break;
   }
   return cudaGetLastError();

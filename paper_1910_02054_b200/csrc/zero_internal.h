@@ -145,6 +145,7 @@ struct AdamArgs {
   float beta1, beta2, eps, omb1, omb2, lrwd;
   int wd;
   const DevState* st;
+  int pdl;                  // host: launch as a programmatic dependent of the preceding kernel
 };
 
 // N_d = 1, a small model: the whole step -- flatten of every bucket with the overflow/norm
