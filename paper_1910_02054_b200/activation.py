@@ -1,6 +1,6 @@
 """Binding of the P_a / P_a+cpu calls (partitioned activation checkpoints, PAPER.md
 §6.1) of include/zero_b200.h: argument marshalling only -- every copy runs
-in the library (k_pa_copy, the copy engines, or NCCL).
+in the library (the engine's k_copy, the copy engines, or NCCL).
 
   PaContext          one MP rank's checkpoint store (zero_pa_init/bind/save/prefetch/gather)
   PaSimGroup         N_m simulated MP ranks on one GPU (zero_pa_sim_group)
