@@ -230,5 +230,5 @@ def test_soak_no_host_sync_one_gpu_per_rank(world, stage, dt, mode):
 @pytest.mark.parametrize("stage", [1, 2])
 def test_ipc_replicated_gradients_at_scale_one_gpu_per_rank(world, stage):
     from test_gpu_ipc import _scale_worker
-    msgs = run_workers(_scale_worker, world, pre=(stage, 4), post=(True,), timeout=900)
+    msgs = run_workers(_scale_worker, world, pre=(stage, 4, "gpt2_1.5b"), post=(True,), timeout=1200)
     assert msgs == ["ok"] * world, msgs
