@@ -7,8 +7,9 @@ them) zero_reduce_grads (flatten/cast/scale + reduce-scatter + overflow/norm
 epilogue), then zero_step (global decision, fused partitioned Adam + recast into
 the all-gather buffer, all-gather); at stage 3 the per-layer gathers of the
 forward and backward as well.  Inputs are resident in HBM when the timed
-region starts; the working set (>= 25 GB) is >> the 126 MB L2, so no L2 flush is
-needed between steps (stated in config.l2).
+region starts.  A working set of >= 25 GB (the GPT layouts) is >> the 126 MB L2, so no
+L2 flush is needed between steps; a small one (config 1, ~32 MB) is timed step by step
+with L2 flushed before each (stated in config.l2).
 
 Default (N=1): the 7.5B layout of the paper's Fig. 1 (Psi = 7,500,000,000,
 120 GB of model states), ZeRO stage 2 (P_os+g), bf16 params/grads with fp32 Adam
@@ -48,6 +49,7 @@ sys.path.insert(0, ROOT)
 METRIC = "ZeRO step Gparams/s at 1/2/4/8 B200; % of HBM+NVLink roofline"
 NVLINK_GBS = 770.0        # per direction per GPU: the measured peer copy (B200_PROFILING.md)
 NVLINK_NOMINAL_GBS = 900.0
+L2_BYTES = 126 << 20        # B200 L2
 DEFAULT_STAGE = {"gpt2_1.5b": 1, "gpt_7.5b": 2, "gpt_60b": 3, "mlp1m": 2}
 # transports with a passing multi-device parity test in this repo's history:
 # the CUDA-IPC PEER path is bit-exact across processes (tests/test_gpu_ipc.py); NCCL at
@@ -81,6 +83,8 @@ def parse():
     ap.add_argument("--graph", action="store_true",
                     help="capture one whole step (all zero_reduce_grads + zero_step) in a CUDA graph and time replays")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--l2-flush", default="auto", choices=["auto", "off"],
+                    help="auto: flush L2 before each timed step when the working set fits in it; off: A/B only")
     ap.add_argument("--no-fp16-key", action="store_true", help="skip the fp16 dynamic-loss-scale second run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cpu-parallel", action="store_true", help="skip the all-cores oracle baseline")
@@ -486,20 +490,35 @@ def main():
                                        (args.phase_events == "auto" and psi_total >= 100_000_000))
         if graph is None and not in_region:
             eng.set_timing(False)
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
         if clocks:
             clocks.mark(True)
-        evs[0].record(stream)
-        for i in range(steps):
-            run_step()
-            evs[i + 1].record(stream)      # per-step boundaries (median / p10 / p90)
+        if flush_buf is None:
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+            evs[0].record(stream)
+            for i in range(steps):
+                run_step()
+                evs[i + 1].record(stream)      # per-step boundaries (median / p10 / p90)
+        else:
+            # the working set fits in L2: every timed step starts from a flushed L2 (a write of
+            # 2x the L2 size between steps, outside the step's event pair)
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(steps)]
+            for i in range(steps):
+                flush_buf.fill_(i & 0xFF)
+                evs[i][0].record(stream)
+                run_step()
+                evs[i][1].record(stream)
         torch.cuda.synchronize()
         if clocks:
             clocks.mark(False)
         barrier()
         comm2 = eng.comm_counters()
-        ms = max_over_ranks(evs[0].elapsed_time(evs[-1]) / steps, dev)
-        per_step = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(steps))
+        if flush_buf is None:
+            ms = max_over_ranks(evs[0].elapsed_time(evs[-1]) / steps, dev)
+            per_step = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(steps))
+        else:
+            per_step = sorted(a.elapsed_time(b) for a, b in evs)
+            ms = max_over_ranks(sum(per_step) / steps, dev)
         clk = clocks.stop() if clocks else None
         tm = eng.timing()
         launches = tm.kernel_launches - launches0 if graph is None else launches_per_step * steps
@@ -531,6 +550,16 @@ def main():
             sent = [getattr(comm1, f) - getattr(comm0, f) for f in ("reduce_scatter", "all_gather", "all_reduce")]
         return {"ms": ms, "per_step": per_step, "tm": tm, "launches": launches, "clocks": clk, "rec": rec,
                 "graph": graph is not None, "sent": sent, "phases": phases, "phase_events": phase_events}
+
+    # bytes one step streams (flatten 4 B + Adam 28 B per parameter): below 4x the L2, flush it
+    flush_buf = None
+    if 32 * psi_total < 4 * L2_BYTES and args.l2_flush == "auto":
+        flush_buf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
+    l2_note = (f"no flush: {32 * psi_total / 1e9:.3g} GB streamed per step vs 126 MB L2"
+               + (" (--l2-flush off: L2-resident A/B, not a contract number)" if args.l2_flush == "off" else "")
+               if flush_buf is None else
+               f"flushed before every timed step ({2 * L2_BYTES >> 20} MB write, outside the step's events): "
+               f"the {32 * psi_total / 1e6:.3g} MB working set fits in the 126 MB L2")
 
     eng, cfg, grad_buf, grads = build(args.dtype)
     info = eng.info
@@ -630,7 +659,7 @@ def main():
                    "adam_state_dtype": "fp32", "reduce_mode": cfg.reduce_mode,
                    "transport": transport, "transport_verified": verified, "parallelism": f"zero{args.stage}-dp{world}",
                    "same_device_ranks": bool(same_dev and world > 1),
-                   "l2": "no flush: >= 25 GB streamed per step vs 126 MB L2"},
+                   "l2": l2_note},
         "roofline": {"bound": "hbm", "kernel": "k_adam (fused partitioned Adam + recast)",
                      "achieved": adam_gbs, "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": adam_gbs / hbm_peak if adam_gbs else None, "traffic": traffic,

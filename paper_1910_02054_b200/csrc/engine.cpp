@@ -1483,6 +1483,7 @@ zero_status issue_adam(zero_ctx* c, ZeroGroup* g) {
   if (!c->adam_variant_env && c->S_e <= c->adam_small) variant = 1;
   if (adam_variant_is_tma(variant) && !c->segs_aligned8) variant = 0;  // bulk copies need 16-B granules
   a.pdl = (c->adam_pdl && variant == 1) ? 1 : 0;   // launch while the whole-step flatten finishes
+  a.aligned8 = c->segs_aligned8 ? 1 : 0;
   c->adam_pdl = false;
   const int grid = grid_for((c->S_e + 2047) / 2048, adam_ctas_per_sm(variant), c->sms);
   a.per_cta = align_up((c->S_e + grid - 1) / grid, 8);

@@ -247,6 +247,20 @@ __device__ void grid_publish(double s, uint32_t f, GridPartials* part, Slot* slo
   }
 }
 
+// the state fields the decision reads, loaded in one batch (independent loads, no branch
+// between them): a caller on a latency-bound path issues them early (flat_decide)
+__device__ __forceinline__ DevSnap snap_state(const DevState* st) {
+  DevSnap s;
+  s.b1t = __ldcg(&st->b1t);
+  s.b2t = __ldcg(&st->b2t);
+  s.t = __ldcg(&st->t);
+  s.S = __ldcg(&st->S);
+  s.good = __ldcg(&st->good);
+  s.inv_cur = __ldcg(&st->inv_cur);
+  return s;
+}
+
+__device__ void decide_apply(double sum, double flags, const DevSnap& s0, DevState* st, const DecideParams& p);
 __device__ void decide_apply(double sum, double flags, DevState* st, const DecideParams& p);
 
 // the last CTA of a whole-step flatten (N_d = 1, every bucket in one launch): sum the per-CTA
@@ -254,7 +268,11 @@ __device__ void decide_apply(double sum, double flags, DevState* st, const Decid
 __device__ __noinline__ void flat_decide(const FlatArgs& a) {
   __shared__ bool is_last;
   __syncthreads();
+  DevSnap snap;
   if (threadIdx.x == 0) {
+    // the state is written only by this launch's last CTA, after every CTA's ticket: the
+    // snapshot's loads overlap the fence and the ticket instead of following the reduction
+    snap = snap_state(a.decide_st);
     __threadfence();
     is_last = atomicAdd(&a.decide_part->ticket, 1u) == gridDim.x - 1;
   }
@@ -272,7 +290,7 @@ __device__ __noinline__ void flat_decide(const FlatArgs& a) {
     a.decide_part->ticket = 0;
     a.decide_out->sumsq = s;
     a.decide_out->flag = f ? 1.0 : 0.0;
-    decide_apply(s, f ? 1.0 : 0.0, a.decide_st, a.decide);
+    decide_apply(s, f ? 1.0 : 0.0, snap, a.decide_st, a.decide);
   }
 }
 
@@ -1453,37 +1471,47 @@ cudaError_t launch_combine_partials(const PartialPtrs& pp, RankPartial* out, cud
 
 // the decision itself (reading c-4), one thread: overflow -> skip + back off the loss
 // scale; else the clip coefficient, t, the bias-correction scalars and the scale growth
-__device__ void decide_apply(double sum, double flags, DevState* st, const DecideParams& p) {
+__device__ void decide_apply(double sum, double flags, const DevSnap& s0, DevState* st, const DecideParams& p) {
   const bool overflow = flags != 0.0;
-  const float S_used = st->S;
+  const float S_used = s0.S;
   const double norm = sqrt(sum);
   float clip = 1.0f;
+  float S = s0.S;
+  uint32_t good = s0.good;
+  uint64_t t = s0.t;
   if (overflow) {
     st->skip = 1u;
     if (p.dynamic) {
-      st->S = fmaxf(st->S * 0.5f, p.min_scale);
-      st->good = 0;
+      S = fmaxf(S * 0.5f, p.min_scale);
+      good = 0;
     }
   } else {
     if (p.max_norm > 0.0f && norm > (double)p.max_norm) clip = (float)((double)p.max_norm / (norm + 1e-6));
-    st->t += 1;
-    st->b1t *= (double)p.beta1;
-    st->b2t *= (double)p.beta2;
-    st->step_f = (float)((double)p.lr / (1.0 - st->b1t));
-    st->rsb2_f = (float)(1.0 / sqrt(1.0 - st->b2t));
+    t += 1;
+    const double b1t = s0.b1t * (double)p.beta1;
+    const double b2t = s0.b2t * (double)p.beta2;
+    st->t = t;
+    st->b1t = b1t;
+    st->b2t = b2t;
+    st->step_f = (float)((double)p.lr / (1.0 - b1t));
+    st->rsb2_f = (float)(1.0 / sqrt(1.0 - b2t));
     st->clip_f = clip;
-    st->inv_adam = st->inv_cur;
+    st->inv_adam = s0.inv_cur;
     st->skip = 0u;
     if (p.dynamic) {
-      st->good += 1;
-      if (st->good == p.window) {
-        st->S = st->S * 2.0f;
-        st->good = 0;
+      good += 1;
+      if (good == p.window) {
+        S = S * 2.0f;
+        good = 0;
       }
     }
   }
-  st->inv_cur = (float)(1.0 / ((double)p.n_ranks * (double)st->S * (double)p.sigma));
-  st->rec_t = st->t;
+  if (p.dynamic) {
+    st->S = S;
+    st->good = good;
+  }
+  st->inv_cur = (float)(1.0 / ((double)p.n_ranks * (double)S * (double)p.sigma));
+  st->rec_t = t;
   st->rec_overflow = overflow ? 1u : 0u;
   st->rec_scale = S_used;
   st->rec_clip = clip;
@@ -1491,13 +1519,17 @@ __device__ void decide_apply(double sum, double flags, DevState* st, const Decid
   st->rec_norm = norm;
   if (p.rec_out) {   // the caller's pinned record, written over PCIe (no D2H copy in the step)
     uint64_t* r = reinterpret_cast<uint64_t*>(p.rec_out);
-    r[0] = st->t;
+    r[0] = t;
     r[1] = (uint64_t)(overflow ? 1u : 0u) | ((uint64_t)__float_as_uint(S_used) << 32);
     r[2] = (uint64_t)__float_as_uint(clip);
     r[3] = (uint64_t)__double_as_longlong(norm);
     // no system fence: the caller reads the record after synchronizing the stream, and a
     // kernel's writes are visible to the host once it has completed
   }
+}
+
+__device__ void decide_apply(double sum, double flags, DevState* st, const DecideParams& p) {
+  decide_apply(sum, flags, snap_state(st), st, p);
 }
 
 __global__ void k_decide_global(const __grid_constant__ PartialPtrs pp, DevState* st, const DecideParams p) {
@@ -1584,19 +1616,9 @@ struct AdamIO {
 // MINB: CTAs per SM the register budget is sized for; U: 8-element groups per
 // thread per iteration (all loads of an iteration are issued before any math).
 template <int PDT, int GDT, int U>
-__device__ __forceinline__ void adam_body(const AdamArgs& a, const AdamScalars& c);
+__device__ __forceinline__ void adam_body(const AdamArgs& a, const AdamScalars& c, uint64_t lo, uint64_t hi);
 
-template <int PDT, int GDT, int MINB, int U>
-__global__ void __launch_bounds__(kThreads, MINB) k_adam(const __grid_constant__ AdamArgs a) {
-  // PDL (a.pdl): launched while the whole-step flatten that made the decision finishes; wait
-  // for it to complete (its writes visible) before reading the decision (a no-op otherwise)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (a.st->skip) return;  // overflow: the whole step is skipped (reading c-4)
-  AdamScalars c;
-  c.inv = a.st->inv_adam;
-  c.step = a.st->step_f;
-  c.rsb2 = a.st->rsb2_f;
-  c.clip = a.st->clip_f;
+__device__ __forceinline__ void adam_scalars(const AdamArgs& a, AdamScalars& c) {
   c.beta1 = a.beta1;
   c.beta2 = a.beta2;
   c.eps = a.eps;
@@ -1604,24 +1626,86 @@ __global__ void __launch_bounds__(kThreads, MINB) k_adam(const __grid_constant__
   c.omb2 = a.omb2;
   c.lrwd = a.lrwd;
   c.wd = a.wd;
-  adam_body<PDT, GDT, U>(a, c);
+}
+
+// index of the segment holding shard element i (segments sorted by local_off, tiling [0, total))
+__device__ __forceinline__ int find_seg(const AdamArgs& a, uint64_t i) {
+  int s0 = 0, s1 = a.n_segs - 1;
+  while (s0 < s1) {
+    const int mid = (s0 + s1 + 1) >> 1;
+    if (a.segs[mid].local_off <= i) s0 = mid; else s1 = mid - 1;
+  }
+  return s0;
+}
+
+template <int PDT, int GDT, int MINB, int U>
+__global__ void __launch_bounds__(kThreads, MINB) k_adam(const __grid_constant__ AdamArgs a) {
+  // PDL (a.pdl): launched while the whole-step flatten that made the decision finishes; wait
+  // for it to complete (its writes visible) before reading the decision (a no-op otherwise)
+  const uint64_t lo = (uint64_t)blockIdx.x * a.per_cta;
+  if (lo >= a.total) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
+  const uint64_t hi = lo + a.per_cta < a.total ? lo + a.per_cta : a.total;
+  AdamScalars c;
+  adam_scalars(a, c);
+  // PDL with 8-aligned segments: the first 8-element group of every thread -- its p32/m/v
+  // (written by no kernel since the previous step's Adam) and its segment -- is fetched
+  // before the wait, so those loads overlap the flatten's tail; only G and the decision
+  // are read after it
+  const uint64_t i0 = lo + threadIdx.x * 8;
+  const bool pre = a.pdl && a.aligned8 && hi - lo >= (uint64_t)kThreads * 8;
+  U8 p, m, v;
+  int64_t gd = 0, pd = 0;
+  if (pre) {
+    p = ld256(a.p32 + i0);
+    m = ld256(a.m + i0);
+    v = ld256(a.v + i0);
+    const AdamSeg sg = a.segs[find_seg(a, i0)];
+    gd = (int64_t)sg.g_off - (int64_t)sg.local_off;
+    pd = (int64_t)sg.p16_off - (int64_t)sg.local_off;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the decision's outputs, all loaded before the skip branch
+  const uint32_t skip = a.st->skip;
+  c.inv = a.st->inv_adam;
+  c.step = a.st->step_f;
+  c.rsb2 = a.st->rsb2_f;
+  c.clip = a.st->clip_f;
+  if (skip) return;  // overflow: the whole step is skipped (reading c-4)
+  if (pre) {
+    using P = H16<PDT>;
+    float G[8];
+    AdamIO<PDT, GDT>::load_g(a.G, i0 + gd, G);
+    U4 o;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float pj = __uint_as_float(p.x[j]), mj = __uint_as_float(m.x[j]), vj = __uint_as_float(v.x[j]);
+      adam_elem(pj, mj, vj, G[j], c);
+      p.x[j] = __float_as_uint(pj);
+      m.x[j] = __float_as_uint(mj);
+      v.x[j] = __float_as_uint(vj);
+      h_set(o, j, P::narrow(pj));
+    }
+    st256(a.p32 + i0, p);
+    st256(a.m + i0, m);
+    st256(a.v + i0, v);
+    for (int d = 0; d < a.n_p16; ++d) st128(reinterpret_cast<uint16_t*>(a.p16[d]) + (i0 + pd), o);
+    adam_body<PDT, GDT, U>(a, c, lo + (uint64_t)kThreads * 8, hi);   // the rest of the range, if any
+  } else {
+    adam_body<PDT, GDT, U>(a, c, lo, hi);
+  }
 }
 
 // the register-staged Adam over this CTA's contiguous range of the shard (k_adam and the
 // fused small-model step)
 template <int PDT, int GDT, int U>
-__device__ __forceinline__ void adam_body(const AdamArgs& a, const AdamScalars& c) {
+__device__ __forceinline__ void adam_body(const AdamArgs& a, const AdamScalars& c, uint64_t lo, uint64_t hi) {
   using P = H16<PDT>;
   using IO = AdamIO<PDT, GDT>;
-  const uint64_t lo = (uint64_t)blockIdx.x * a.per_cta;
-  if (lo >= a.total) return;
-  const uint64_t hi = lo + a.per_cta < a.total ? lo + a.per_cta : a.total;
-  // first segment containing lo (segments sorted by local_off, tiling [0, total))
-  int s0 = 0, s1 = a.n_segs - 1;
-  while (s0 < s1) {
-    const int mid = (s0 + s1 + 1) >> 1;
-    if (a.segs[mid].local_off <= lo) s0 = mid; else s1 = mid - 1;
-  }
+  if (lo >= hi) return;
+  const int s0 = find_seg(a, lo);   // first segment containing lo
   uint64_t cur = lo;
   for (int s = s0; cur < hi && s < a.n_segs; ++s) {
     const AdamSeg sg = a.segs[s];
@@ -2129,14 +2213,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_step_small(const __grid_constan
   c.step = __ldcg(&a.st->step_f);
   c.rsb2 = __ldcg(&a.st->rsb2_f);
   c.clip = __ldcg(&a.st->clip_f);
-  c.beta1 = a.adam.beta1;
-  c.beta2 = a.adam.beta2;
-  c.eps = a.adam.eps;
-  c.omb1 = a.adam.omb1;
-  c.omb2 = a.adam.omb2;
-  c.lrwd = a.adam.lrwd;
-  c.wd = a.adam.wd;
-  adam_body<DDT, DDT, 1>(a.adam, c);
+  adam_scalars(a.adam, c);
+  const uint64_t lo = (uint64_t)blockIdx.x * a.adam.per_cta;
+  if (lo >= a.adam.total) return;
+  adam_body<DDT, DDT, 1>(a.adam, c, lo, lo + a.adam.per_cta < a.adam.total ? lo + a.adam.per_cta : a.adam.total);
 }
 
 template <int SD, int DD, bool CP>

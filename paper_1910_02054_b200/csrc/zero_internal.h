@@ -54,6 +54,15 @@ struct DevState {
   double rec_norm;
 };
 
+// the DevState fields the decision reads (decide_apply), loaded together
+struct DevSnap {
+  double b1t, b2t;
+  uint64_t t;
+  float S;
+  uint32_t good;
+  float inv_cur;
+};
+
 struct DecideParams {
   int n_ranks;
   int dynamic;
@@ -146,6 +155,7 @@ struct AdamArgs {
   int wd;
   const DevState* st;
   int pdl;                  // host: launch as a programmatic dependent of the preceding kernel
+  int aligned8;             // every segment's local_off, count, g_off and p16_off % 8 == 0
 };
 
 // N_d = 1, a small model: the whole step -- flatten of every bucket with the overflow/norm
