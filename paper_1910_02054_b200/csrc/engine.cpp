@@ -201,6 +201,8 @@ struct zero_ctx {
   bool flat_cta_partials = true;                   // ZERO_FLAT_CTA_PARTIALS=0: last-CTA combine in each flatten
   bool rs_cta_partials = true;                     // ZERO_RS_CTA_PARTIALS=0: last-CTA combine in each reduce-scatter
   int rs_ctas = 4, rs_u = 0;                       // ZERO_RS_CTAS (CTAs per SM), ZERO_RS_U (0 = per-N default)
+  int rs_grid = 0;                                 // ZERO_RS_GRID: cap on the pull's CTAs per launch (0 = none;
+                                                   // an NVLink-bound pull needs few SMs: the sweep knob for NVL8)
   int rs_pipe = 1;                                 // ZERO_RS_PIPE: 1 = software-pipelined pull (default), 0 = plain
   bool rs_multi = true;                            // ZERO_RS_MULTI=0: simulated ranks' pulls launched per rank
   // ZeRO x MP (R-MP1): per-slot norm weights (0 for MP-replicated buckets on MP rank > 0)
@@ -427,7 +429,8 @@ int rs_setup(const zero_ctx* c, uint32_t k, RSArgs& a, uint64_t sl) {
   }
   a.u = c->rs_u;
   a.pipe = c->rs_pipe;
-  return grid_for((sl + 2047) / 2048, c->rs_ctas, c->sms);
+  const int g = grid_for((sl + 2047) / 2048, c->rs_ctas, c->sms);
+  return c->rs_grid > 0 ? std::min(g, c->rs_grid) : g;   // grid-stride body: any grid is exact
 }
 
 DecideParams decide_params(const zero_ctx* c);
@@ -795,6 +798,7 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   if (const char* ev = getenv("ZERO_RS_CTA_PARTIALS")) c->rs_cta_partials = atoi(ev) != 0;
   c->rs_ctas = c->n_d == 8 ? 3 : 4;   // the pipelined pull at N_d = 8 holds 78 registers: 3 CTAs/SM
   if (const char* ev = getenv("ZERO_RS_CTAS")) c->rs_ctas = std::max(1, std::min(8, atoi(ev)));
+  if (const char* ev = getenv("ZERO_RS_GRID")) c->rs_grid = std::max(0, std::min(kMaxGrid, atoi(ev)));
   if (const char* ev = getenv("ZERO_RS_U")) c->rs_u = atoi(ev);
   if (const char* ev = getenv("ZERO_RS_PIPE")) c->rs_pipe = atoi(ev);
   if (const char* ev = getenv("ZERO_RS_MULTI")) c->rs_multi = atoi(ev) != 0;

@@ -30,6 +30,8 @@ VARIANTS = {
     "rs_plain_u1_c6": {"ZERO_RS_PIPE": "0", "ZERO_RS_U": "1", "ZERO_RS_CTAS": "6"},
     "rs_w16": {"ZERO_RS_PIPE": "2"},
     "rs_w16_pipe": {"ZERO_RS_PIPE": "3", "ZERO_RS_CTAS": "2"},
+    "rs_grid_cap": {"ZERO_RS_GRID": "5"},                         # a few CTAs, grid-stride (NVLink-bound sizing)
+    "rs_grid_cap_per_rank": {"ZERO_RS_GRID": "3", "ZERO_RS_MULTI": "0"},
     "flat_grid_combine": {"ZERO_FLAT_CTA_PARTIALS": "0", "ZERO_SMALL_BUCKET": "0"},
     "step_small_fused": {"ZERO_STEP_SMALL": "1"},
 }
