@@ -201,6 +201,8 @@ struct zero_ctx {
   bool flat_cta_partials = true;                   // ZERO_FLAT_CTA_PARTIALS=0: last-CTA combine in each flatten
   bool rs_cta_partials = true;                     // ZERO_RS_CTA_PARTIALS=0: last-CTA combine in each reduce-scatter
   int rs_ctas = 4, rs_u = 0;                       // ZERO_RS_CTAS (CTAs per SM), ZERO_RS_U (0 = per-N default)
+  int gather_grid = 0;                             // ZERO_GATHER_GRID: cap on a stage-3 layer gather's CTAs per
+                                                   // source rank (0 = none; NVLink-bound, overlaps the forward)
   int rs_grid = 0;                                 // ZERO_RS_GRID: cap on the pull's CTAs per launch (0 = none;
                                                    // an NVLink-bound pull needs few SMs: the sweep knob for NVL8)
   int rs_pipe = 1;                                 // ZERO_RS_PIPE: 1 = software-pipelined pull (default), 0 = plain
@@ -799,6 +801,7 @@ zero_status zero_bind_buffers(zero_ctx* c, const zero_buffers* b) {
   c->rs_ctas = c->n_d == 8 ? 3 : 4;   // the pipelined pull at N_d = 8 holds 78 registers: 3 CTAs/SM
   if (const char* ev = getenv("ZERO_RS_CTAS")) c->rs_ctas = std::max(1, std::min(8, atoi(ev)));
   if (const char* ev = getenv("ZERO_RS_GRID")) c->rs_grid = std::max(0, std::min(kMaxGrid, atoi(ev)));
+  if (const char* ev = getenv("ZERO_GATHER_GRID")) c->gather_grid = std::max(0, std::min(kMaxGrid, atoi(ev)));
   if (const char* ev = getenv("ZERO_RS_U")) c->rs_u = atoi(ev);
   if (const char* ev = getenv("ZERO_RS_PIPE")) c->rs_pipe = atoi(ev);
   if (const char* ev = getenv("ZERO_RS_MULTI")) c->rs_multi = atoi(ev) != 0;
@@ -1952,7 +1955,9 @@ zero_status issue_layer_gather(zero_ctx* c, int li, int slot) {
       }
       for (int j = 0; j < c->n_d; ++j) a.count[j] = sl;
       a.n = c->n_d;
-      CK(launch_copy(a, grid_for((sl + 2047) / 2048, 2, c->sms), gst));
+      int grid = grid_for((sl + 2047) / 2048, 2, c->sms);
+      if (c->gather_grid > 0) grid = std::min(grid, c->gather_grid);   // grid-stride copy: any grid is exact
+      CK(launch_copy(a, grid, gst));
       c->launches++;
       c->counters.all_gather += sl * (uint64_t)(c->n_d - 1);
     }

@@ -32,6 +32,7 @@ VARIANTS = {
     "rs_w16_pipe": {"ZERO_RS_PIPE": "3", "ZERO_RS_CTAS": "2"},
     "rs_grid_cap": {"ZERO_RS_GRID": "5"},                         # a few CTAs, grid-stride (NVLink-bound sizing)
     "rs_grid_cap_per_rank": {"ZERO_RS_GRID": "3", "ZERO_RS_MULTI": "0"},
+    "gather_grid_cap": {"ZERO_GATHER_GRID": "2"},                # stage-3 layer gathers on 2 CTAs per source
     "flat_grid_combine": {"ZERO_FLAT_CTA_PARTIALS": "0", "ZERO_SMALL_BUCKET": "0"},
     "step_small_fused": {"ZERO_STEP_SMALL": "1"},
 }
