@@ -3,7 +3,7 @@
 # line + reference arm, config 1 (flushed / warm), its ncu launch list, the sanitizers
 set -x
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-O=gpurun_out/final2
+O=gpurun_out/${FINAL_DIR:-final2}
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $O/gpu.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
